@@ -1,0 +1,319 @@
+"""Benchmark: stable-sorted 64-bit keys/s on B200 vs the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+One step = one full stable sort (keys + payload) of the configured workload.
+N=1 default workload: BASELINE config 2 (10^7 float64 N(0,1) keys, seed 1,
+int32 original-index payload), the config BASELINE.json's metric is quoted
+on.  Inputs are resident in HBM for `value`; `e2e` times the public API on
+pinned host buffers (H2D + sort + D2H inside the timed region).  L2 is
+flushed (512 MiB write) between timed steps, outside the timed region.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+C restatement in oracle/, single-threaded like the reference) on the host,
+same workload and metric.  Under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "stable-sorted 64-bit keys/sec at 1/2/4/8 B200; achieved HBM GB/s vs roofline"
+CONFIG_DESC = {
+    1: "C1: 1e6 int64 uniform full range (seed 0), int32 index payload",
+    2: "C2: 1e7 float64 N(0,1) (seed 1), int32 index payload",
+    3: "C3: 1e7 int64 from 1000 distinct values in [0,2^40) (seed 2), int32 index payload",
+    4: "C4: 1e8 float64 lognormal(0,2) half + sorted half with 1% swaps (seed 3), int32 index payload",
+    5: "C5: 2^31/N int64 per GPU (uniform, 10% one repeated value, seed 4), int64 index payload",
+    9: "X9: 1e9 int64 uniform full range (seed 9), int32 index payload",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_workload(cfg: int, rank: int = 0, world: int = 1):
+    """Host arrays (keys, payload) for one rank."""
+    from oracle import oracle as O
+
+    if cfg in (1, 2, 3, 4):
+        return O.make_config(cfg)
+    if cfg == 9:
+        keys = np.random.default_rng(9).integers(-(2**63), 2**63 - 1, size=10**9, endpoint=True, dtype=np.int64)
+        return keys, np.arange(keys.size, dtype=np.int32)
+    raise ValueError(cfg)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_reference(args, rank: int):
+    """CPU arm: the reference algorithm's C restatement on the host (1 core)."""
+    from oracle import oracle as O
+
+    keys, payload = make_workload(args.config)
+    n = keys.size
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        O.stable_sort(keys[: min(n, 10**6)], payload[: min(n, 10**6)])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.stable_sort(keys, payload)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64" if keys.dtype == np.int64 else "f64",
+        "data": "synthetic", "config": {"workload": CONFIG_DESC[args.config], "n": int(n), "payload_bytes": 4},
+        "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "port",
+                         "sample": f"full workload ({n} keys) x {len(times)} steps; reference algorithm is "
+                                   f"single-threaded by design (SPEC.md:222-223); host cpu_count={os.cpu_count()}"},
+        "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(keys, payload, budget_s=12.0, max_reps=5):
+    from oracle import oracle as O
+
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_reps and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        O.stable_sort(keys, payload)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": keys.size / med, "unit": "keys/s", "cores": 1, "kind": "port",
+            "sample": f"full workload ({keys.size} keys), median of {len(times)} runs of the oracle restatement "
+                      f"(oracle/zsort_oracle.c) on this host; cpu_count={os.cpu_count()}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--mapping", default="fitted", choices=["fitted", "paper"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, rank)
+        return
+
+    import torch
+
+    import paper_2605_14419_b200 as Z
+    from paper_2605_14419_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.load()
+    keys_h, pay_h = make_workload(args.config, rank, world)
+    n = keys_h.size
+    pb = pay_h.dtype.itemsize
+    kd = 1 if keys_h.dtype == np.float64 else 0
+    cfg = Z.SortConfig(mapping=args.mapping)
+    c = cfg.to_c()
+    d_keys = torch.from_numpy(keys_h).to(dev)
+    d_pay = torch.from_numpy(pay_h).to(dev)
+    out_k = torch.empty_like(d_keys)
+    out_p = torch.empty_like(d_pay)
+    ws_bytes = L.zsb_workspace_bytes(n, kd, pb, c)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    import ctypes
+
+    stats = (ctypes.c_int64 * 5)()
+
+    def sort_once():
+        rc = L.zsb_sort(d_keys.data_ptr(), kd, d_pay.data_ptr(), pb, out_k.data_ptr(), out_p.data_ptr(), n, c,
+                        ws.data_ptr(), ws_bytes, stats, stream.cuda_stream)
+        _lib.check(rc)
+
+    for _ in range(max(3, args.warmup)):
+        sort_once()
+    torch.cuda.synchronize()
+    # correctness gate on the benchmarked output (device structural check)
+    idx = d_pay.to(torch.int64) if pb == 4 else d_pay
+    viol = Z.check_stable_permutation_device(d_keys, out_k, out_p)
+    if viol:
+        raise SystemExit(f"benchmarked output failed the structural check: {viol} violations")
+
+    ms_phase = (ctypes.c_double * 8)()
+    launches = (ctypes.c_int64 * 8)()
+    L.zsb_timing_read(ms_phase, launches, 8, 1)
+    L.zsb_timing_enable(1)
+    step_ms = []
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sort_once()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    L.zsb_timing_enable(0)
+    L.zsb_timing_read(ms_phase, launches, 8, 1)
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n * world / (ms_per_step / 1e3)
+
+    hbm_peak, peak_kind = peaks()
+    rec = 8 + pb
+    alg_bytes_step = {"moments": 8 * n, "histogram": 8 * n, "scan": None, "scatter": 2 * rec * n,
+                      "classify": None, "finish": 2 * rec * n, "recursion_stats": None, "misc": None}
+    phase_ms = {name: ms_phase[i] / args.steps for i, name in enumerate(_lib.PHASES)}
+    phase_launch = {name: launches[i] / args.steps for i, name in enumerate(_lib.PHASES)}
+    dominant = max(("moments", "histogram", "scatter", "finish"), key=lambda k: phase_ms[k])
+    per_launch_bytes = alg_bytes_step[dominant] / max(1.0, phase_launch[dominant])
+    per_launch_ms = phase_ms[dominant] / max(1.0, phase_launch[dominant])
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    sort_alg_bytes = (16 + 4 * rec) * n
+    gpu_launches = int(sum(launches[i] for i in range(8)))
+    line = {
+        "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64" if kd == 1 else "int64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[args.config], "n_per_gpu": int(n), "payload_bytes": pb,
+                   "mapping": args.mapping, "l2": "flushed (512 MiB write) between timed steps",
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "kernel": f"k_{dominant}", "achieved": achieved, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_ms},
+        "sort_roofline": {"alg_bytes_per_key": 16 + 4 * rec, "achieved_gbs": sort_alg_bytes / (ms_per_step / 1e3) / 1e9,
+                          "frac": sort_alg_bytes / (ms_per_step / 1e3) / 1e9 / hbm_peak},
+        "phases_ms_per_step": {k: round(v, 4) for k, v in phase_ms.items()},
+        "gpu_launches": gpu_launches,
+        "stats": {"max_depth": stats[0], "fallbacks": stats[1], "finish_runs": stats[3], "scatters": stats[4]},
+    }
+    line["clocks"] = clk.summary()
+
+    if not args.no_e2e:
+        hk = torch.from_numpy(keys_h).pin_memory()
+        hp = torch.from_numpy(pay_h).pin_memory()
+        for _ in range(2):
+            Z.zsort(hk, hp, cfg)
+        e2e_ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ok, op, _ = Z.zsort(hk, hp, cfg)
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+        e2e_step = sum(e2e_ms) / len(e2e_ms)
+        line["e2e"] = {"value": n * world / (e2e_step / 1e3), "unit": "keys/s",
+                       "h2d_bytes_per_step": int(n * rec), "d2h_bytes_per_step": int(n * rec),
+                       "ms_per_step": e2e_step, "api": "paper_2605_14419_b200.zsort(pinned host tensors)"}
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(keys_h, pay_h)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

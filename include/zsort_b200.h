@@ -1,0 +1,144 @@
+/*
+ * zsort_b200.h -- C ABI of the B200-native stable z-score partitioning sort.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (arxiv 2605.14419, Python package `zsort`) has no C ABI of its own: its
+ * native boundary is the numba dispatcher call
+ *     _kernels.zsort_driver(src_k, src_c, out_k, out_c, scr_k, scr_c, k,
+ *                           scale, mean, std, zmin, insertion_limit,
+ *                           counting_limit, depth_guard, counters)
+ * (/root/reference/pkg/src/zsort/_kernels.py:393-396) reached from
+ * core.zsort (core.py:348-400).  The entry points below replace that
+ * boundary with plain pointers and sizes; every pointer named d_* is CUDA
+ * device memory owned by the caller, and every call is stream-ordered on the
+ * given cudaStream_t (passed as void* so this header needs no CUDA include).
+ *
+ * Conventions (mirroring the reference):
+ *  - inputs are never modified (core.py:351-352);
+ *  - outputs and workspace are caller-allocated; kernels never allocate
+ *    (_kernels.py:3-5);
+ *  - no global mutable state: calls on different streams/workspaces are
+ *    independent (reentrant);
+ *  - return 0 on success or a ZSB_ERR_* code; zsb_last_error() gives a
+ *    thread-local message.  The Python wrapper maps ZSB_ERR_ARG/ZSB_ERR_NAN
+ *    to ValueError and ZSB_ERR_DTYPE to TypeError, like core.py:151-181.
+ */
+#ifndef ZSORT_B200_H
+#define ZSORT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Key element types.  The reference accepts only signed integers
+ * (core.py:151-165); float64 is a documented extension (NaN rejected). */
+typedef enum { ZSB_KEY_I64 = 0, ZSB_KEY_F64 = 1 } zsb_key_dtype;
+
+/* Bucket mapping for partition levels.
+ *  ZSB_MAP_FITTED: z-score mapping whose scale is fitted to the segment's
+ *                  z-range (GPU default: balanced buckets, fewer levels);
+ *  ZSB_MAP_PAPER:  the paper's Eq. 1 exactly, scale = k/4 with
+ *                  k = max(2, round(alpha*sqrt(n))) (core.py:146-148,233-234).
+ * Both produce the identical (unique) stable order. */
+typedef enum { ZSB_MAP_FITTED = 0, ZSB_MAP_PAPER = 1 } zsb_mapping;
+
+/* Mirror of SortConfig (core.py:63-89) plus the GPU mapping choice. */
+typedef struct {
+    double alpha;                     /* (0, 2]; paper-mode bucket count */
+    int64_t insertion_threshold;      /* n <= this: one shared-memory finish */
+    int64_t counting_range_threshold; /* accepted for API parity */
+    int64_t depth_guard;              /* >= 3: levels before the exact bit split */
+    int32_t collect_stats;            /* accepted; counters are always kept */
+    int32_t mapping;                  /* zsb_mapping */
+} zsb_config;
+
+/* SortStats slots (core.py:135-143, _kernels.py:16-21). */
+enum {
+    ZSB_STAT_MAX_DEPTH = 0,
+    ZSB_STAT_FALLBACKS = 1,
+    ZSB_STAT_COUNTING = 2,
+    ZSB_STAT_INSERTION = 3,
+    ZSB_STAT_SCATTERS = 4,
+    ZSB_STAT_SLOTS = 5
+};
+
+enum {
+    ZSB_OK = 0,
+    ZSB_ERR_ARG = 1,       /* bad size/pointer/config (ValueError) */
+    ZSB_ERR_DTYPE = 2,     /* unsupported key or payload type (TypeError) */
+    ZSB_ERR_NAN = 3,       /* NaN key (ValueError) */
+    ZSB_ERR_WORKSPACE = 4, /* workspace too small */
+    ZSB_ERR_CUDA = 5       /* CUDA launch/runtime failure (RuntimeError) */
+};
+
+/* Bytes of device workspace zsb_sort needs for n keys.
+ * Replaces the scratch arrays allocated at core.py:367-368,393-394. */
+size_t zsb_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, const zsb_config *cfg);
+
+/* Stable ascending sort of n 8-byte keys with an optional 4- or 8-byte
+ * payload (payload_bytes 0/4/8; d_payload/d_out_payload may be NULL when 0).
+ * Replaces core.zsort -> _kernels.zsort_driver (core.py:348-400,
+ * _kernels.py:393-450).  h_stats (may be NULL) receives ZSB_STAT_SLOTS
+ * int64 counters; the call blocks until the sort has completed. */
+int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
+             void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
+             int64_t *h_stats, void *stream);
+
+/* Grid-wide moments of n keys (north-star subsystem 1; replaces
+ * first_pass + variance_pass, _kernels.py:28-71, core.py:184-234).
+ * h_out[0..7] = count, mean, M2 (sum of squared deviations around the mean),
+ * min, max (as doubles), 0, 0, NaN count.  h_limbs[0..1] = the exact int64
+ * key sum as first_pass limbs (value = hi*2^32 + lo; int64 keys only), and
+ * h_min_max_bits[0..1] = the raw 8-byte min and max keys.  The mean of int64
+ * keys is the correctly rounded quotient of the exact sum (core.py:226).
+ * Uses the front of a zsb_workspace_bytes(n, ...) workspace; blocks. */
+int zsb_moments(const void *d_keys, int32_t key_dtype, int64_t n, void *d_workspace, size_t workspace_bytes,
+                double *h_out, int64_t *h_limbs, uint64_t *h_min_max_bits, void *stream);
+
+/* Parameter-injected bucket histogram (north-star subsystem 2; replaces
+ * histogram_pass/build_partition_plan, _kernels.py:91-112, core.py:248-256):
+ * params = {mean, std, zmin, scale}; d_counts receives k int64 counts. */
+int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k,
+                  int64_t *d_counts, void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* Parameter-injected one-level stable scatter into bucket order
+ * (north-star subsystems 3+4; replaces exclusive_offsets + scatter_pass,
+ * _kernels.py:115-133, core.py:259-276). */
+int zsb_scatter(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, int64_t n,
+                const double *params, int64_t k, void *d_out_keys, void *d_out_payload, void *d_workspace,
+                size_t workspace_bytes, void *stream);
+
+/* Structural stable-permutation check on the device (K8; replaces
+ * verify.check_stable_permutation, verify.py:55-108, for the case
+ * payload = original index): returns through h_result the number of
+ * violations of (sorted, permutation, key match, stability); 0 = stable.
+ * d_index is int64 (index_bytes 8) or int32 (4); d_in_keys is the unsorted
+ * input.  Needs zsb_check_workspace_bytes(n) of workspace. */
+size_t zsb_check_workspace_bytes(int64_t n);
+int zsb_check_sorted(const void *d_in_keys, const void *d_out_keys, const void *d_index, int32_t index_bytes,
+                     int32_t key_dtype, int64_t n, int64_t index_base, void *d_workspace, int64_t *h_result,
+                     void *stream);
+
+/* Optional per-phase device timing of zsb_sort on the calling thread (CUDA
+ * events around each launch group, on the sort's own stream).  Phase slots:
+ * 0 moments, 1 histogram, 2 scan, 3 scatter, 4 classify+plan, 5 finish,
+ * 6 recursion moments+params, 7 misc.  zsb_timing_read fills up to nslots
+ * accumulated milliseconds and kernel-launch counts (launch counts are kept
+ * even when timing is off) and returns the number of slots. */
+void zsb_timing_enable(int32_t on);
+int32_t zsb_timing_read(double *ms, int64_t *launches, int32_t nslots, int32_t reset);
+
+/* Thread-local message for the last failing call. */
+const char *zsb_last_error(void);
+
+/* Build/version string (compile flags and target arch). */
+const char *zsb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZSORT_B200_H */

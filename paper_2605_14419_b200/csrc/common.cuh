@@ -1,0 +1,185 @@
+// common.cuh -- shared device helpers for the B200 zSort kernels.
+//
+// Keys are moved as raw 8-byte words (int64 or float64 bit patterns); every
+// comparison goes through an order-preserving uint64 image (ord_key) and
+// every z-score evaluation through the key's fp64 value (key_value), so the
+// output keys are bit-identical to the input words.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace zsb {
+
+constexpr uint64_t SIGN = 0x8000000000000000ull;
+constexpr int WARP = 32;
+
+enum KeyKind { KEY_I64 = 0, KEY_F64 = 1 };
+
+// Partition mapping mode of one segment.
+enum SegMode : int32_t {
+    MODE_ZSCORE = 0,   // Eq. 1 z-score bucket (fp64, IEEE-exact intrinsics)
+    MODE_INTEGER = 1,  // exact MSD digit of (ord(key) - ord(min)): termination fallback (K7)
+    MODE_COPY = 2,     // all keys equal: copy through (core.py:377-380, _kernels.py:339-343)
+};
+
+// Per-segment partition parameters (one partition problem of the batch).
+// Level 1 is a batch of one segment covering the whole input.
+struct SegParams {
+    double center;     // mean (level 1) or estimated center (recursion), core.py:226 / _kernels.py:103-106
+    double std;        // sqrt(mean squared deviation around center)
+    double zmin;       // z-offset of the segment minimum
+    double scale;      // buckets per z unit
+    uint64_t umin;     // ordered image of the segment minimum (integer mode)
+    int64_t start;     // first position of the segment in the array
+    int64_t len;       // records in the segment
+    int64_t tile_first;// first tile (CTA) of this segment in the batch
+    int64_t mat_base;  // first entry of this segment's bucket-major count matrix
+    int64_t scan_base; // sum of len over the preceding segments of the batch
+    int64_t tile_len;  // records per tile (last tile may be shorter)
+    int32_t k;         // buckets
+    int32_t ntiles;    // tiles
+    int32_t mode;      // SegMode
+    int32_t level;     // partition depth (1 = first level)
+    int32_t shift;     // integer mode: digit = (ord - umin) >> shift
+    int32_t src;       // buffer holding the segment: 0 = input, 1 = tmp, 2 = out
+};
+
+// Per-segment accumulator for the recursion moments pass (fused_stats_pass,
+// _kernels.py:74-88): ordered min/max and sum of squared deviations.
+struct SegAcc {
+    unsigned long long omin;
+    unsigned long long omax;
+    double s2;
+    double pad;
+};
+
+// Finish work item: a contiguous run of whole buckets, <= capacity records.
+struct Entry {
+    int64_t start;
+    int32_t len;
+    int32_t src;  // 1 = tmp, 2 = out, 0 = input
+};
+
+// Control block slots (uint64).
+enum Ctrl {
+    C_MOM_TICKET = 0,
+    C_SCAN_TICKET = 1,
+    C_NCHILD = 2,
+    C_NENTRY = 3,
+    C_TILES_NEXT = 4,
+    C_MAT_NEXT = 5,
+    C_ST_FALLBACKS = 6,
+    C_ST_SCATTERS = 7,
+    C_ST_MAXDEPTH = 8,
+    C_STATUS = 9,
+    C_ST_INSERTION = 10,
+    C_KMAX_NEXT = 11,
+    C_NEXT_BIG = 12,
+    C_SLOTS = 16
+};
+
+// ------------------------------------------------------------ key traits
+
+template <int KK>
+__device__ __forceinline__ uint64_t ord_key(uint64_t b) {
+    if constexpr (KK == KEY_I64) {
+        return b ^ SIGN;
+    } else {
+        if (b == SIGN) b = 0;  // -0.0 == +0.0
+        return (b & SIGN) ? ~b : (b | SIGN);
+    }
+}
+
+template <int KK>
+__device__ __forceinline__ double key_value(uint64_t b) {
+    if constexpr (KK == KEY_I64) {
+        return __ll2double_rn((long long)b);  // numba int64 -> float64 (round to nearest)
+    } else {
+        return __longlong_as_double((long long)b);
+    }
+}
+
+template <int KK>
+__device__ __forceinline__ uint64_t key_from_ord(uint64_t o) {
+    if constexpr (KK == KEY_I64) {
+        return o ^ SIGN;
+    } else {
+        return (o & SIGN) ? (o ^ SIGN) : ~o;
+    }
+}
+
+// Eq. 1 (_kernels.py:91-100) with explicit round-to-nearest intrinsics so
+// nvcc cannot contract or reassociate: identical to the reference's
+// sequential IEEE evaluation.
+__device__ __forceinline__ int32_t bucket_z(double x, double center, double std, double zmin, double scale,
+                                            int32_t k) {
+    double h = __dmul_rn(__dadd_rn(__ddiv_rn(__dsub_rn(x, center), std), zmin), scale);
+    double f = floor(h);
+    if (!(f > 0.0)) return 0;
+    if (f >= (double)k) return k - 1;
+    return (int32_t)f;
+}
+
+template <int KK>
+__device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p) {
+    if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
+    if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
+    return 0;
+}
+
+// ---------------------------------------------------------- warp helpers
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+// Named barriers 1..15 (0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int PB>
+struct PayloadT {
+    using T = uint32_t;
+};
+template <>
+struct PayloadT<8> {
+    using T = uint64_t;
+};
+
+__device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
+
+}  // namespace zsb

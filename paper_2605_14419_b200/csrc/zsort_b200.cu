@@ -1,0 +1,694 @@
+// zsort_b200.cu -- host orchestration and the C ABI (include/zsort_b200.h).
+//
+// zsb_sort replaces core.zsort -> _kernels.zsort_driver -> _run_worklist
+// (core.py:348-400, _kernels.py:321-450).  One partition level is the
+// launch sequence  K1 moments -> K2 hist -> K3 scan -> K4 scatter -> classify
+// -> plan, all on the caller's stream; the host reads back one small control
+// block per level (how many oversized buckets recurse, how many finish runs
+// to launch), then launches K5 over that level's finish runs.  Recursion
+// levels batch every oversized bucket of the previous level into one
+// segmented launch (device-side segment table, no per-segment host work).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/zsort_b200.h"
+#include "kernels.cuh"
+
+using namespace zsb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+// ---- optional per-phase device timing (CUDA events on the sort's stream)
+enum Phase { PH_MOMENTS = 0, PH_HIST, PH_SCAN, PH_SCATTER, PH_CLASSIFY, PH_FINISH, PH_SEGSTATS, PH_MISC, PH_SLOTS };
+
+struct Timing {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<int> slot_of;  // per recorded pair
+    size_t used = 0;
+    double ms[PH_SLOTS] = {0};
+    long long launches[PH_SLOTS] = {0};
+    long long launch_total = 0;
+};
+thread_local Timing g_t;
+
+struct PhaseScope {
+    int slot;
+    cudaStream_t st;
+    bool active;
+    PhaseScope(int s, cudaStream_t stream, int nlaunch = 1) : slot(s), st(stream), active(g_t.on) {
+        g_t.launch_total += nlaunch;
+        g_t.launches[s] += nlaunch;
+        if (!active) return;
+        if (g_t.used + 2 > g_t.pool.size()) {
+            for (int i = 0; i < 64; i++) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                g_t.pool.push_back(e);
+            }
+        }
+        cudaEventRecord(g_t.pool[g_t.used], st);
+    }
+    ~PhaseScope() {
+        if (!active) return;
+        cudaEventRecord(g_t.pool[g_t.used + 1], st);
+        g_t.slot_of.push_back(slot);
+        g_t.used += 2;
+    }
+};
+
+// after a stream sync: fold recorded pairs into the per-phase totals
+void timing_collect() {
+    if (!g_t.on) return;
+    for (size_t i = 0; i < g_t.slot_of.size(); i++) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, g_t.pool[2 * i], g_t.pool[2 * i + 1]) == cudaSuccess) g_t.ms[g_t.slot_of[i]] += ms;
+    }
+    g_t.slot_of.clear();
+    g_t.used = 0;
+}
+
+#define ZSB_CUDA(call)                                                                                  \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(ZSB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+#define ZSB_LAUNCH(what)                                                                                \
+    do {                                                                                                \
+        cudaError_t e_ = cudaGetLastError();                                                            \
+        if (e_ != cudaSuccess) return fail(ZSB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+constexpr int SB_MAX = 2048;      // finish sub-buckets
+constexpr int K_LEVEL1_MAX = 49152;  // cursor smem 192 KB
+constexpr int KMAX_CHILD = 8192;
+constexpr int MIN_TILE = 8192;
+
+int finish_cap(int pb) { return pb == 8 ? 7168 : 8192; }
+
+int64_t cluster_count(int64_t n, double alpha) {  // core.py:146-148
+    double v = std::nearbyint(alpha * std::sqrt((double)n));
+    int64_t k = (int64_t)v;
+    return k < 2 ? 2 : k;
+}
+
+int64_t pow2_at_least(int64_t x) {
+    int64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Level-1 plan: bucket count and tiling of the whole input.
+struct Plan1 {
+    int64_t k, tile_len, ntiles, cap, half;
+};
+
+Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
+    Plan1 P;
+    P.cap = finish_cap(pb);
+    P.half = P.cap / 2;
+    if (cfg.mapping == ZSB_MAP_PAPER) {
+        P.k = std::min<int64_t>(cluster_count(n, cfg.alpha), K_LEVEL1_MAX);
+    } else {
+        int64_t kmax = env_int("ZSB_K1MAX", 8192);
+        P.k = std::min<int64_t>(std::max<int64_t>(16, pow2_at_least((4 * n + P.cap - 1) / P.cap)), kmax);
+    }
+    int64_t target_tiles = (int64_t)num_sms() * env_int("ZSB_TILES_PER_SM", 2);
+    int64_t tl = std::max<int64_t>(4 * P.k, (n + target_tiles - 1) / target_tiles);
+    tl = std::max<int64_t>(tl, 2048);
+    tl = (tl + 255) & ~(int64_t)255;
+    P.tile_len = tl;
+    P.ntiles = (n + tl - 1) / tl;
+    return P;
+}
+
+struct Layout {
+    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, entries, parts, ctrl, dbg, total;
+    int64_t mat_cap, seg_cap, ent_cap, status_cap;
+};
+
+constexpr int MOM_GRID_PER_SM = 4;
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
+    Layout L;
+    const int64_t cap = P.cap;
+    L.mat_cap = std::max<int64_t>(P.k * P.ntiles, n / 4 + 24 * (n / cap + 1) + 4096) + 16;
+    L.seg_cap = n / cap + 4;
+    L.ent_cap = 2 * (n / P.half + 1) + 24 * (n / cap + 1) + P.k + 4096;
+    L.status_cap = L.mat_cap / SCAN_TILE + 4;
+    size_t o = 0;
+    L.tmp_k = o;
+    if (need_tmp) o = align_up(o + (size_t)n * 8);
+    L.tmp_p = o;
+    if (need_tmp) o = align_up(o + (size_t)n * pb);
+    L.mat = o;
+    o = align_up(o + (size_t)L.mat_cap * 4);
+    L.status = o;
+    o = align_up(o + (size_t)L.status_cap * 8);
+    L.seg_a = o;
+    o = align_up(o + (size_t)L.seg_cap * sizeof(SegParams));
+    L.seg_b = o;
+    o = align_up(o + (size_t)L.seg_cap * sizeof(SegParams));
+    L.acc = o;
+    o = align_up(o + (size_t)L.seg_cap * sizeof(SegAcc));
+    L.kfirst = o;
+    o = align_up(o + (size_t)(L.seg_cap + 2) * 8);
+    L.entries = o;
+    o = align_up(o + (size_t)L.ent_cap * sizeof(Entry));
+    L.parts = o;
+    o = align_up(o + (size_t)num_sms() * MOM_GRID_PER_SM * sizeof(MomPartial));
+    L.ctrl = o;
+    o = align_up(o + C_SLOTS * 8);
+    L.dbg = o;
+    o = align_up(o + 16 * 8);
+    L.total = o;
+    return L;
+}
+
+template <typename F>
+void smem_optin(F *func, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+__global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t n, int64_t k, int64_t tile_len,
+                              int64_t ntiles, int src, double center, double sd, double zmin, double scale,
+                              int mode) {
+    SegParams p{};
+    p.center = center;
+    p.std = sd;
+    p.zmin = zmin;
+    p.scale = scale;
+    p.start = 0;
+    p.len = n;
+    p.tile_first = 0;
+    p.mat_base = 0;
+    p.scan_base = 0;
+    p.tile_len = tile_len;
+    p.k = (int32_t)k;
+    p.ntiles = (int32_t)ntiles;
+    p.mode = mode;
+    p.level = 1;
+    p.src = src;
+    *seg = p;
+    kfirst[0] = 0;
+    kfirst[1] = k;
+}
+
+__global__ void k_bucket_totals(const uint32_t *mat, int64_t k, int64_t ntiles, int64_t *counts) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= k) return;
+    int64_t s = 0;
+    for (int64_t t = 0; t < ntiles; t++) s += mat[b * ntiles + t];
+    counts[b] = s;
+}
+
+struct Ctx {
+    Buffers B;
+    unsigned char *ws;
+    Layout L;
+    Plan1 P;
+    cudaStream_t st;
+    int64_t n;
+};
+
+template <int KK, int PB>
+int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel) {
+    uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
+    unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+    unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
+    size_t kbytes = (size_t)kmax * 4;
+    smem_optin(k_hist<KK>, kbytes);
+    {
+        PhaseScope ph(PH_HIST, c.st);
+        k_hist<KK><<<(unsigned)tiles, NT, kbytes, c.st>>>(c.B, segs, nseg, mat);
+    }
+    ZSB_LAUNCH("k_hist");
+    int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
+    ZSB_CUDA(cudaMemsetAsync(status, 0, (size_t)(sblocks + 1) * 8, c.st));
+    ZSB_CUDA(cudaMemsetAsync(ctrl + C_SCAN_TICKET, 0, 8, c.st));
+    {
+        PhaseScope ph(PH_SCAN, c.st);
+        k_scan<<<(unsigned)sblocks, NT, 0, c.st>>>(mat, mat_entries, status, ctrl);
+    }
+    ZSB_LAUNCH("k_scan");
+    constexpr int ITEMS = 4;
+    smem_optin(k_scatter<KK, PB, ITEMS>, kbytes);
+    {
+        PhaseScope ph(PH_SCATTER, c.st);
+        k_scatter<KK, PB, ITEMS><<<(unsigned)tiles, NT, kbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel);
+    }
+    ZSB_LAUNCH("k_scatter");
+    return ZSB_OK;
+}
+
+template <int KK, int PB>
+int launch_finish(Ctx &c, int64_t nentries) {
+    if (nentries <= 0) return ZSB_OK;
+    FinLayout FL = fin_layout((int)c.P.cap, PB, SB_MAX);
+    smem_optin(k_finish<KK, PB>, FL.total);
+    Entry *entries = (Entry *)(c.ws + c.L.entries);
+    {
+        PhaseScope ph(PH_FINISH, c.st);
+        k_finish<KK, PB><<<(unsigned)nentries, NT, FL.total, c.st>>>(c.B, entries, (int)c.P.cap, SB_MAX);
+    }
+    ZSB_LAUNCH("k_finish");
+    return ZSB_OK;
+}
+
+template <int KK, int PB>
+int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
+    const int64_t n = c.n;
+    unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+    SegParams *seg_cur = (SegParams *)(c.ws + c.L.seg_a);
+    SegParams *seg_next = (SegParams *)(c.ws + c.L.seg_b);
+    SegAcc *acc = (SegAcc *)(c.ws + c.L.acc);
+    int64_t *kfirst = (int64_t *)(c.ws + c.L.kfirst);
+    Entry *entries = (Entry *)(c.ws + c.L.entries);
+    uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
+    int64_t stats[ZSB_STAT_SLOTS] = {0, 0, 0, 0, 0};
+    ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
+
+    if (n <= c.P.cap) {  // one shared-memory finish (core.py:369-374; threshold widened to the smem capacity)
+        {
+            PhaseScope ph(PH_MISC, c.st);
+            k_single_entry<<<1, 1, 0, c.st>>>(entries, n);
+        }
+        ZSB_LAUNCH("k_single_entry");
+        int rc = launch_finish<KK, PB>(c, 1);
+        if (rc) return rc;
+        ZSB_CUDA(cudaStreamSynchronize(c.st));
+        timing_collect();
+        stats[ZSB_STAT_INSERTION] = 1;
+        if (h_stats) memcpy(h_stats, stats, sizeof(stats));
+        return ZSB_OK;
+    }
+
+    MapCfg mc{cfg.mapping, (int32_t)cfg.depth_guard};
+    ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping};
+    {
+        PhaseScope ph(PH_MISC, c.st);
+        k_init_level1<<<1, 1, 0, c.st>>>(seg_cur, kfirst, n, c.P.k, c.P.tile_len, c.P.ntiles, 0, 0.0, 1.0, 0.0, 1.0,
+                                         MODE_ZSCORE);
+    }
+    ZSB_LAUNCH("k_init_level1");
+    int grid = std::max(1, std::min<int>(num_sms() * MOM_GRID_PER_SM, (int)((n + NT - 1) / NT)));
+    {
+        PhaseScope ph(PH_MOMENTS, c.st);
+        k_moments<KK><<<grid, NT, 0, c.st>>>(c.B.in_k, n, (MomPartial *)(c.ws + c.L.parts), ctrl, seg_cur, mc,
+                                             nullptr);
+    }
+    ZSB_LAUNCH("k_moments");
+
+    int nseg = 1;
+    int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_buckets = c.P.k;
+    int kmax = (int)c.P.k;
+    int level = 1;
+    unsigned long long h_ctrl[C_SLOTS];
+    while (true) {
+        if (level > 1) {
+            {
+                PhaseScope ph(PH_SEGSTATS, c.st, 2);
+                k_seg_moments<KK><<<(unsigned)tiles, NT, 0, c.st>>>(c.B, seg_cur, nseg, acc);
+                k_seg_params<KK><<<(nseg + 127) / 128, 128, 0, c.st>>>(seg_cur, nseg, acc, mc, ctrl);
+            }
+            ZSB_LAUNCH("k_seg_moments/params");
+        }
+        const int dst_sel = (level == 1) ? 1 : ((level % 2 == 0) ? 2 : 1);
+        int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel);
+        if (rc) return rc;
+        ZSB_CUDA(cudaMemsetAsync(ctrl + C_NCHILD, 0, 16, c.st));  // C_NCHILD, C_NENTRY
+        {
+            PhaseScope ph(PH_CLASSIFY, c.st, 2);
+            k_classify<<<(unsigned)((total_buckets + 255) / 256), 256, 0, c.st>>>(
+                seg_cur, nseg, kfirst, mat, entries, seg_next, acc, ctrl, cc, total_buckets);
+            k_plan<<<1, 1024, 0, c.st>>>(seg_next, ctrl + C_NCHILD, kfirst, ctrl, cfg.mapping, (int32_t)c.P.cap,
+                                         KMAX_CHILD, MIN_TILE);
+        }
+        ZSB_LAUNCH("k_classify/k_plan");
+        ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
+        ZSB_CUDA(cudaStreamSynchronize(c.st));
+        timing_collect();
+        if (h_ctrl[C_STATUS] == 3) return fail(ZSB_ERR_NAN, "NaN keys have no order");
+        int64_t nentry = (int64_t)h_ctrl[C_NENTRY];
+        if (nentry > c.L.ent_cap) return fail(ZSB_ERR_WORKSPACE, "finish entry list overflow");
+        int rc2 = launch_finish<KK, PB>(c, nentry);
+        if (rc2) return rc2;
+        stats[ZSB_STAT_INSERTION] += nentry;
+        int64_t nchild = (int64_t)h_ctrl[C_NCHILD];
+        if (nchild == 0) break;
+        if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
+        nseg = (int)nchild;
+        tiles = (int64_t)h_ctrl[C_TILES_NEXT];
+        mat_entries = (int64_t)h_ctrl[C_MAT_NEXT];
+        kmax = (int)h_ctrl[C_KMAX_NEXT];
+        total_buckets = (int64_t)h_ctrl[C_NEXT_BIG];
+        if (mat_entries > c.L.mat_cap) return fail(ZSB_ERR_WORKSPACE, "count matrix overflow");
+        std::swap(seg_cur, seg_next);
+        level++;
+        if (level > 200) return fail(ZSB_ERR_CUDA, "partition did not terminate");
+    }
+    ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
+    ZSB_CUDA(cudaStreamSynchronize(c.st));
+    timing_collect();
+    stats[ZSB_STAT_MAX_DEPTH] = (int64_t)h_ctrl[C_ST_MAXDEPTH];
+    stats[ZSB_STAT_FALLBACKS] = (int64_t)h_ctrl[C_ST_FALLBACKS];
+    stats[ZSB_STAT_SCATTERS] = (int64_t)h_ctrl[C_ST_SCATTERS];
+    if (h_stats) memcpy(h_stats, stats, sizeof(stats));
+    return ZSB_OK;
+}
+
+int check_common(const void *d_keys, int32_t kd, int32_t pb, int64_t n) {
+    if (kd != ZSB_KEY_I64 && kd != ZSB_KEY_F64) return fail(ZSB_ERR_DTYPE, "key dtype must be int64 or float64");
+    if (pb != 0 && pb != 4 && pb != 8) return fail(ZSB_ERR_DTYPE, "payload must be 0, 4 or 8 bytes wide");
+    if (n < 0) return fail(ZSB_ERR_ARG, "n must be >= 0");
+    if (n >= ((int64_t)1 << 32)) return fail(ZSB_ERR_ARG, "n must be < 2^32 per device");
+    if (n > 0 && !d_keys) return fail(ZSB_ERR_ARG, "null key pointer");
+    return ZSB_OK;
+}
+
+zsb_config default_cfg() {
+    zsb_config c;
+    c.alpha = 0.6;
+    c.insertion_threshold = 96;
+    c.counting_range_threshold = 65000;
+    c.depth_guard = 32;
+    c.collect_stats = 0;
+    c.mapping = ZSB_MAP_FITTED;
+    return c;
+}
+
+int check_cfg(const zsb_config &c) {  // core.py:81-89
+    if (!(c.alpha > 0 && c.alpha <= 2)) return fail(ZSB_ERR_ARG, "alpha must be in (0, 2]");
+    if (c.insertion_threshold < 1) return fail(ZSB_ERR_ARG, "insertion_threshold must be >= 1");
+    if (c.counting_range_threshold < 1) return fail(ZSB_ERR_ARG, "counting_range_threshold must be >= 1");
+    if (c.depth_guard < 3) return fail(ZSB_ERR_ARG, "depth_guard must be >= 3");
+    if (c.mapping != ZSB_MAP_FITTED && c.mapping != ZSB_MAP_PAPER) return fail(ZSB_ERR_ARG, "bad mapping");
+    return ZSB_OK;
+}
+
+template <template <int, int> class F, typename... A>
+int dispatch(int kd, int pb, A &&...args) {
+    if (kd == ZSB_KEY_I64) {
+        if (pb == 0) return F<0, 0>::run(args...);
+        if (pb == 4) return F<0, 4>::run(args...);
+        return F<0, 8>::run(args...);
+    }
+    if (pb == 0) return F<1, 0>::run(args...);
+    if (pb == 4) return F<1, 4>::run(args...);
+    return F<1, 8>::run(args...);
+}
+
+template <int KK, int PB>
+struct SortOp {
+    static int run(Ctx &c, const zsb_config &cfg, int64_t *h_stats) { return run_sort<KK, PB>(c, cfg, h_stats); }
+};
+
+// -------------------------------------------------------------- K8 check
+
+template <int KK, typename IT>
+__global__ void k_check(const uint64_t *in_k, const uint64_t *out_k, const IT *idx, int64_t n, int64_t base,
+                        unsigned int *bitmap, unsigned long long *viol) {
+    unsigned long long bad = 0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = (int64_t)idx[j] - base;
+        uint64_t ok = ord_key<KK>(out_k[j]);
+        if (p < 0 || p >= n) {
+            bad++;
+            continue;
+        }
+        unsigned bit = 1u << (p & 31);
+        unsigned old = atomicOr(&bitmap[p >> 5], bit);
+        if (old & bit) bad++;                      // repeated index: not a permutation
+        if (in_k[p] != out_k[j]) bad++;            // key does not belong to that index
+        if (j > 0) {
+            uint64_t pk = ord_key<KK>(out_k[j - 1]);
+            if (ok < pk) bad++;                                           // not sorted
+            if (ok == pk && (int64_t)idx[j] <= (int64_t)idx[j - 1]) bad++;  // not stable
+        }
+    }
+    bad = warp_sum(bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(viol, bad);
+}
+
+int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_payload, int32_t pb, int64_t n,
+                          const double *params, int64_t k, void *d_out_keys, void *d_out_payload, void *d_workspace,
+                          size_t workspace_bytes, void *stream) {
+    int rc = check_common(d_keys, kd, pb, n);
+    if (rc) return rc;
+    if (n < 1 || k < 2 || k > K_LEVEL1_MAX || !params)
+        return fail(ZSB_ERR_ARG, "need n >= 1, 2 <= k <= 49152 and params");
+    if (!(params[1] > 0.0) || !(params[3] > 0.0)) return fail(ZSB_ERR_ARG, "std and scale must be positive");
+    ctx.n = n;
+    ctx.P.k = k;
+    ctx.P.cap = finish_cap(pb);
+    ctx.P.half = ctx.P.cap / 2;
+    int64_t target = (int64_t)num_sms() * 2;
+    int64_t tl = std::max<int64_t>(std::max<int64_t>(4 * k, 2048), (n + target - 1) / target);
+    ctx.P.tile_len = (tl + 255) & ~(int64_t)255;
+    ctx.P.ntiles = (n + ctx.P.tile_len - 1) / ctx.P.tile_len;
+    ctx.L = make_layout(n, pb, ctx.P, false);
+    if (!d_workspace || workspace_bytes < ctx.L.total) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
+    ctx.ws = (unsigned char *)d_workspace;
+    ctx.st = (cudaStream_t)stream;
+    ctx.B.in_k = (const uint64_t *)d_keys;
+    ctx.B.in_p = d_payload;
+    ctx.B.tmp_k = nullptr;
+    ctx.B.tmp_p = nullptr;
+    ctx.B.out_k = (uint64_t *)d_out_keys;
+    ctx.B.out_p = d_out_payload;
+    SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
+    int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
+    k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0], params[1],
+                                       params[2], params[3], MODE_ZSCORE);
+    ZSB_LAUNCH("k_init_level1");
+    return ZSB_OK;
+}
+
+template <int KK, int PB>
+struct ScatterOp {
+    static int run(Ctx &c) {
+        SegParams *seg = (SegParams *)(c.ws + c.L.seg_a);
+        unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+        cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st);
+        int rc = launch_partition<KK, PB>(c, seg, 1, c.P.ntiles, c.P.k * c.P.ntiles, (int)c.P.k, 2);
+        if (rc) return rc;
+        ZSB_CUDA(cudaStreamSynchronize(c.st));
+        return ZSB_OK;
+    }
+};
+
+}  // namespace
+
+// ================================================================== C ABI
+
+extern "C" {
+
+const char *zsb_last_error(void) { return g_err.c_str(); }
+
+void zsb_timing_enable(int32_t on) {
+    g_t.on = on != 0;
+    g_t.slot_of.clear();
+    g_t.used = 0;
+}
+
+int32_t zsb_timing_read(double *ms, int64_t *launches, int32_t nslots, int32_t reset) {
+    int k = nslots < PH_SLOTS ? nslots : PH_SLOTS;
+    for (int i = 0; i < k; i++) {
+        if (ms) ms[i] = g_t.ms[i];
+        if (launches) launches[i] = g_t.launches[i];
+    }
+    if (reset) {
+        for (int i = 0; i < PH_SLOTS; i++) {
+            g_t.ms[i] = 0;
+            g_t.launches[i] = 0;
+        }
+        g_t.launch_total = 0;
+    }
+    return PH_SLOTS;
+}
+
+const char *zsb_version(void) {
+    return "zsort_b200 0.1 (sm_100a; K1 moments, K2 hist, K3 lookback scan, K4 token-ring stable scatter, "
+           "K5 smem finish)";
+}
+
+size_t zsb_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, const zsb_config *cfg) {
+    (void)key_dtype;
+    zsb_config c = cfg ? *cfg : default_cfg();
+    if (n < 1) n = 1;
+    Plan1 P = plan_level1(n, payload_bytes, c);
+    return make_layout(n, payload_bytes, P, true).total;
+}
+
+int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
+             void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
+             int64_t *h_stats, void *stream) {
+    int rc = check_common(d_keys, key_dtype, payload_bytes, n);
+    if (rc) return rc;
+    zsb_config c = cfg ? *cfg : default_cfg();
+    rc = check_cfg(c);
+    if (rc) return rc;
+    if (h_stats) memset(h_stats, 0, sizeof(int64_t) * ZSB_STAT_SLOTS);
+    if (n == 0) return ZSB_OK;
+    if (!d_out_keys || (payload_bytes && (!d_payload || !d_out_payload)))
+        return fail(ZSB_ERR_ARG, "null output or payload pointer");
+    Ctx ctx;
+    ctx.n = n;
+    ctx.P = plan_level1(n, payload_bytes, c);
+    ctx.L = make_layout(n, payload_bytes, ctx.P, true);
+    if (!d_workspace || workspace_bytes < ctx.L.total) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
+    ctx.ws = (unsigned char *)d_workspace;
+    ctx.st = (cudaStream_t)stream;
+    ctx.B.in_k = (const uint64_t *)d_keys;
+    ctx.B.in_p = d_payload;
+    ctx.B.tmp_k = (uint64_t *)(ctx.ws + ctx.L.tmp_k);
+    ctx.B.tmp_p = ctx.ws + ctx.L.tmp_p;
+    ctx.B.out_k = (uint64_t *)d_out_keys;
+    ctx.B.out_p = d_out_payload;
+    return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats);
+}
+
+int zsb_moments(const void *d_keys, int32_t key_dtype, int64_t n, void *d_workspace, size_t workspace_bytes,
+                double *h_out, int64_t *h_limbs, uint64_t *h_min_max_bits, void *stream) {
+    int rc = check_common(d_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    if (n < 1) return fail(ZSB_ERR_ARG, "moments require a nonempty segment");
+    size_t need = align_up((size_t)num_sms() * MOM_GRID_PER_SM * sizeof(MomPartial)) + align_up(sizeof(SegParams)) +
+                  align_up(C_SLOTS * 8) + align_up(16 * 8);
+    if (!d_workspace || workspace_bytes < need) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
+    unsigned char *ws = (unsigned char *)d_workspace;
+    MomPartial *parts = (MomPartial *)ws;
+    SegParams *seg = (SegParams *)(ws + align_up((size_t)num_sms() * MOM_GRID_PER_SM * sizeof(MomPartial)));
+    unsigned long long *ctrl = (unsigned long long *)((unsigned char *)seg + align_up(sizeof(SegParams)));
+    double *dbg = (double *)((unsigned char *)ctrl + align_up(C_SLOTS * 8));
+    cudaStream_t st = (cudaStream_t)stream;
+    ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, st));
+    ZSB_CUDA(cudaMemsetAsync(seg, 0, sizeof(SegParams), st));
+    int grid = std::max(1, std::min<int>(num_sms() * MOM_GRID_PER_SM, (int)((n + NT - 1) / NT)));
+    MapCfg mc{ZSB_MAP_FITTED, 32};
+    if (key_dtype == ZSB_KEY_I64)
+        k_moments<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, parts, ctrl, seg, mc, dbg);
+    else
+        k_moments<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, parts, ctrl, seg, mc, dbg);
+    ZSB_LAUNCH("k_moments");
+    double h[16];
+    ZSB_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    ZSB_CUDA(cudaStreamSynchronize(st));
+    if (h_out) {
+        for (int i = 0; i < 8; i++) h_out[i] = h[i];
+        h_out[5] = h_out[6] = 0.0;
+    }
+    if (h_limbs) memcpy(h_limbs, &h[8], 16);
+    if (h_min_max_bits) memcpy(h_min_max_bits, &h[10], 16);
+    return ZSB_OK;
+}
+
+int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k,
+                  int64_t *d_counts, void *d_workspace, size_t workspace_bytes, void *stream) {
+    Ctx ctx;
+    int rc = injected_setup(ctx, d_keys, key_dtype, nullptr, 0, n, params, k, nullptr, nullptr, d_workspace,
+                            workspace_bytes, stream);
+    if (rc) return rc;
+    SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
+    uint32_t *mat = (uint32_t *)(ctx.ws + ctx.L.mat);
+    size_t kb = (size_t)k * 4;
+    if (key_dtype == ZSB_KEY_I64) {
+        smem_optin(k_hist<0>, kb);
+        k_hist<0><<<(unsigned)ctx.P.ntiles, NT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
+    } else {
+        smem_optin(k_hist<1>, kb);
+        k_hist<1><<<(unsigned)ctx.P.ntiles, NT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
+    }
+    ZSB_LAUNCH("k_hist");
+    k_bucket_totals<<<(unsigned)((k + 255) / 256), 256, 0, ctx.st>>>(mat, k, ctx.P.ntiles, d_counts);
+    ZSB_LAUNCH("k_bucket_totals");
+    ZSB_CUDA(cudaStreamSynchronize(ctx.st));
+    return ZSB_OK;
+}
+
+int zsb_scatter(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, int64_t n,
+                const double *params, int64_t k, void *d_out_keys, void *d_out_payload, void *d_workspace,
+                size_t workspace_bytes, void *stream) {
+    Ctx ctx;
+    int rc = injected_setup(ctx, d_keys, key_dtype, d_payload, payload_bytes, n, params, k, d_out_keys,
+                            d_out_payload, d_workspace, workspace_bytes, stream);
+    if (rc) return rc;
+    return dispatch<ScatterOp>(key_dtype, payload_bytes, ctx);
+}
+
+size_t zsb_check_workspace_bytes(int64_t n) { return align_up((size_t)((n + 31) / 32) * 4) + 256; }
+
+int zsb_check_sorted(const void *d_in_keys, const void *d_out_keys, const void *d_index, int32_t index_bytes,
+                     int32_t key_dtype, int64_t n, int64_t index_base, void *d_workspace, int64_t *h_result,
+                     void *stream) {
+    int rc = check_common(d_in_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    if (index_bytes != 4 && index_bytes != 8) return fail(ZSB_ERR_DTYPE, "index must be int32 or int64");
+    if (n == 0) {
+        if (h_result) *h_result = 0;
+        return ZSB_OK;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned int *bitmap = (unsigned int *)d_workspace;
+    size_t bm = align_up((size_t)((n + 31) / 32) * 4);
+    unsigned long long *viol = (unsigned long long *)((unsigned char *)d_workspace + bm);
+    ZSB_CUDA(cudaMemsetAsync(d_workspace, 0, bm + 8, st));
+    int grid = num_sms() * 8;
+    if (key_dtype == ZSB_KEY_I64) {
+        if (index_bytes == 8)
+            k_check<0, long long><<<grid, 256, 0, st>>>((const uint64_t *)d_in_keys, (const uint64_t *)d_out_keys,
+                                                      (const long long *)d_index, n, index_base, bitmap, viol);
+        else
+            k_check<0, int><<<grid, 256, 0, st>>>((const uint64_t *)d_in_keys, (const uint64_t *)d_out_keys,
+                                                (const int *)d_index, n, index_base, bitmap, viol);
+    } else {
+        if (index_bytes == 8)
+            k_check<1, long long><<<grid, 256, 0, st>>>((const uint64_t *)d_in_keys, (const uint64_t *)d_out_keys,
+                                                      (const long long *)d_index, n, index_base, bitmap, viol);
+        else
+            k_check<1, int><<<grid, 256, 0, st>>>((const uint64_t *)d_in_keys, (const uint64_t *)d_out_keys,
+                                                (const int *)d_index, n, index_base, bitmap, viol);
+    }
+    ZSB_LAUNCH("k_check");
+    unsigned long long h = 0;
+    ZSB_CUDA(cudaMemcpyAsync(&h, viol, 8, cudaMemcpyDeviceToHost, st));
+    ZSB_CUDA(cudaStreamSynchronize(st));
+    if (h_result) *h_result = (int64_t)h;
+    return ZSB_OK;
+}
+
+}  // extern "C"
