@@ -197,12 +197,14 @@ def _np_payload_kind(arr: np.ndarray) -> int:
 
 # ----------------------------------------------------------------- zsort
 
-def zsort(keys, payload=None, config: SortConfig | None = None):
+def zsort(keys, payload=None, config: SortConfig | None = None, *, out=None):
     """Stably sort records by key on the GPU; returns ``(keys, payload, stats)``.
 
     Drop-in for core.zsort (core.py:348-400): inputs are never modified and
     new arrays are returned.  numpy inputs give numpy outputs (host round
     trip included); torch tensors give torch tensors on the input's device.
+    ``out=(keys_out, payload_out)`` (torch tensors, e.g. pinned host buffers)
+    receives the result instead of fresh allocations (extension).
     """
     cfg = config if config is not None else SortConfig()
     kt, kind = _coerce_keys(keys)
@@ -257,6 +259,13 @@ def zsort(keys, payload=None, config: SortConfig | None = None):
                         ws.data_ptr(), ws_bytes, stats, _stream_ptr(dev))
         _lib.check(rc)
         st = SortStats(*[int(x) for x in stats])
+        if out is not None and kind == "torch" and gather_src is None:
+            ok_t, op_t = out
+            ok_t.copy_(out_k, non_blocking=ok_t.is_pinned())
+            if op_t is not None and out_p is not None:
+                op_t.copy_(out_p, non_blocking=op_t.is_pinned())
+            torch.cuda.current_stream(dev).synchronize()
+            return ok_t, op_t, st
         res_p = None
         if payload is not None:
             if gather_src is not None:

@@ -76,6 +76,9 @@ enum Ctrl {
     C_ST_INSERTION = 10,
     C_KMAX_NEXT = 11,
     C_NEXT_BIG = 12,
+    C_WIN_NEXT = 13,
+    C_NREF0 = 14,
+    C_NREF1 = 15,
     C_SLOTS = 16
 };
 

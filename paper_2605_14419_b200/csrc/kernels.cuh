@@ -396,26 +396,15 @@ __global__ void __launch_bounds__(NT) k_hist(Buffers B, const SegParams *__restr
     for (int b = threadIdx.x; b < p.k; b += NT) hist[b] = 0;
     __syncthreads();
     const uint64_t *src = src_keys(B, p.src);
-    const int lane = lane_id();
-    // warp-uniform trip counts: every lane reaches each __match_any_sync
-    int64_t i0 = t0 + (threadIdx.x & ~31);
-    for (; i0 + 3 * NT + 31 < t1; i0 += 4 * NT) {
-        uint64_t b[4];
+    int64_t i = t0 + threadIdx.x;
+    for (; i + 7 * NT < t1; i += 8 * NT) {
+        uint64_t b[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++) b[u] = __ldcs(src + i0 + u * NT + lane);
+        for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * NT);
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            int32_t bk = seg_bucket<KK>(b[u], p);
-            unsigned peers = __match_any_sync(0xffffffffu, bk);
-            if ((peers & lanemask_lt()) == 0) atomicAdd(&hist[bk], (uint32_t)__popc(peers));
-        }
+        for (int u = 0; u < 8; u++) atomicAdd(&hist[seg_bucket<KK>(b[u], p)], 1u);
     }
-    for (; i0 < t1; i0 += NT) {
-        int64_t i = i0 + lane;
-        int32_t bk = i < t1 ? seg_bucket<KK>(__ldcs(src + i), p) : -1;
-        unsigned peers = __match_any_sync(0xffffffffu, bk);
-        if (bk >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(&hist[bk], (uint32_t)__popc(peers));
-    }
+    for (; i < t1; i += NT) atomicAdd(&hist[seg_bucket<KK>(__ldcs(src + i), p)], 1u);
     __syncthreads();
     for (int b = threadIdx.x; b < p.k; b += NT) col[(int64_t)b * p.ntiles] = hist[b];
 }
@@ -508,22 +497,89 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 // ------------------------------------------------------------------- K4
 // Stable scatter.  Each CTA owns one tile (a contiguous input range) and
 // starts from its column of the scanned count matrix, so tiles land in
-// input order inside every bucket.  Inside the CTA the 8 warps take turns
-// (a token ring over named barriers) to advance the per-bucket cursors in
-// shared memory, and inside a warp equal-bucket keys are ranked by
-// __match_any_sync + popc(peers & lanemask_lt): every record keeps its input
-// order within its bucket (_kernels.py:124-133 front-to-back semantics).
+// input order inside every bucket.  The tile is processed in rounds of
+// NT*ITEMS records; each round is stably sorted by bucket in shared memory:
+//   count  warp w owns the contiguous slice [w*32*ITEMS, (w+1)*32*ITEMS) of
+//          the round; equal-bucket keys are ranked with __match_any_sync and
+//          the leaders advance per-(bucket, warp) u16 counters;
+//   scan   exclusive scan of the counters in (bucket, warp) order;
+//   place  records go to shared memory at their stable local position;
+//   write  thread i stores staged record i to cursor[b] + (i - run_start[b]):
+//          consecutive threads write consecutive addresses of each bucket run
+//          (coalesced), then the bucket cursors advance by the run lengths.
+// Every record keeps its input order within its bucket, the front-to-back
+// semantics of scatter_pass (_kernels.py:124-133), with no cross-warp
+// serialization.
 
-template <int KK, int PB, int ITEMS>
-__global__ void __launch_bounds__(NT) k_scatter(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                                const uint32_t *__restrict__ mat, int dst_sel) {
+constexpr int SCAT_ITEMS = 16;
+constexpr int SCAT_ROUND = NT * SCAT_ITEMS;  // 4096 records per round
+constexpr int KSCAT_MAX = 2048;             // fan-out limit of one pass
+
+struct ScatLayout {
+    size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, total;
+};
+
+__host__ __device__ inline ScatLayout scat_layout(int k, int pb) {
+    ScatLayout L;
+    size_t o = 0;
+    L.off_cur = o;
+    o += (size_t)k * 4;
+    L.off_cnt = o;
+    o += (size_t)k * NWARPS * 2;
+    o = (o + 15) & ~(size_t)15;
+    L.off_lst = o;
+    o += (size_t)(k + 1) * 2;
+    o = (o + 15) & ~(size_t)15;
+    L.off_k = o;
+    o += (size_t)SCAT_ROUND * 8;
+    L.off_p = o;
+    o += (size_t)SCAT_ROUND * pb;
+    o = (o + 15) & ~(size_t)15;
+    L.off_b = o;
+    o += (size_t)SCAT_ROUND * 2;
+    L.total = (o + 15) & ~(size_t)15;
+    return L;
+}
+
+// Exclusive scan of n u16 counters in place (n a multiple of 32*NWARPS is
+// not required; any n), warp-cooperative, conflict-free; returns nothing.
+__device__ __forceinline__ void block_scan_u16(uint16_t *c, int n, uint32_t *wtot) {
+    const int w = threadIdx.x >> 5, lane = lane_id();
+    const int chunk = ((n + NWARPS * 32 - 1) / (NWARPS * 32)) * 32;
+    const int lo = w * chunk, hi = min(n, lo + chunk);
+    uint32_t tot = 0;
+    for (int q = lo + lane; q < hi; q += 32) tot += c[q];
+    tot = warp_sum(tot);
+    if (lane == 0) wtot[w] = tot;
+    __syncthreads();
+    uint32_t run = 0;
+    for (int q = 0; q < w; q++) run += wtot[q];
+    for (int j0 = lo; j0 < hi; j0 += 32) {
+        const int q = j0 + lane;
+        uint32_t v = q < hi ? c[q] : 0u, x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (q < hi) c[q] = (uint16_t)(run + x - v);
+        run += __shfl_sync(0xffffffffu, x, 31);
+    }
+    __syncthreads();
+}
+
+template <int KK, int PB>
+__global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *__restrict__ segs, int nseg,
+                                                   const uint32_t *__restrict__ mat, int dst_sel) {
     using P = typename PayloadT<PB>::T;
-    extern __shared__ uint32_t cur[];
+    constexpr int ITEMS = SCAT_ITEMS;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t wtot[NWARPS];
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
-    int64_t ti = blockIdx.x - p.tile_first;
-    int64_t t0 = p.start + ti * p.tile_len;
-    int64_t t1 = min(t0 + p.tile_len, p.start + p.len);
+    const int64_t ti = blockIdx.x - p.tile_first;
+    const int64_t t0 = p.start + ti * p.tile_len;
+    const int64_t t1 = min(t0 + p.tile_len, p.start + p.len);
     const uint64_t *sk = src_keys(B, p.src);
     const P *sp = src_pay<PB>(B, p.src);
     if (p.mode == MODE_COPY) {  // all-equal segment: land it in the output directly
@@ -535,177 +591,214 @@ __global__ void __launch_bounds__(NT) k_scatter(Buffers B, const SegParams *__re
         }
         return;
     }
+    const int k = p.k;
+    const ScatLayout L = scat_layout(k, PB);
+    uint32_t *cur = (uint32_t *)(smem + L.off_cur);
+    uint16_t *cnt = (uint16_t *)(smem + L.off_cnt);
+    uint16_t *lst = (uint16_t *)(smem + L.off_lst);
+    uint64_t *stk = (uint64_t *)(smem + L.off_k);
+    P *stp = (P *)(smem + L.off_p);
+    uint16_t *stb = (uint16_t *)(smem + L.off_b);
     uint64_t *dk = dst_sel == 1 ? B.tmp_k : B.out_k;
     P *dp = (P *)(dst_sel == 1 ? B.tmp_p : B.out_p);
     const uint32_t *col = mat + p.mat_base + ti;
     const uint32_t adj = (uint32_t)(p.start - p.scan_base);
-    for (int b = threadIdx.x; b < p.k; b += NT) cur[b] = col[(int64_t)b * p.ntiles] + adj;
+    const int NC = k * NWARPS;
+    for (int b = threadIdx.x; b < k; b += NT) cur[b] = col[(int64_t)b * p.ntiles] + adj;
+    for (int q = threadIdx.x; q < NC; q += NT) cnt[q] = 0;
     __syncthreads();
 
     const int w = threadIdx.x >> 5, lane = lane_id();
     const unsigned lt = lanemask_lt();
-    constexpr int R = NT * ITEMS;
-    const int64_t nr = (t1 - t0 + R - 1) / R;
-    for (int64_t r = 0; r < nr; r++) {
-        const int64_t base = t0 + r * R + (int64_t)w * (32 * ITEMS) + lane;
+    for (int64_t r0 = t0; r0 < t1; r0 += SCAT_ROUND) {
+        const int nvalid = (int)min((int64_t)SCAT_ROUND, t1 - r0);
+        const int base = w * 32 * ITEMS + lane;
         uint64_t key[ITEMS];
         P pay[ITEMS];
-        int32_t bk[ITEMS];
-        unsigned peers[ITEMS];
+        int bk[ITEMS];
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            int64_t idx = base + j * 32;
-            bool v = idx < t1;
-            key[j] = v ? __ldcs(sk + idx) : 0ull;
-            if constexpr (PB != 0) pay[j] = v ? __ldcs(sp + idx) : (P)0;
-            bk[j] = v ? seg_bucket<KK>(key[j], p) : -1;
+            const int i = base + j * 32;
+            key[j] = i < nvalid ? __ldcs(sk + r0 + i) : 0ull;
+            if constexpr (PB != 0) pay[j] = i < nvalid ? __ldcs(sp + r0 + i) : (P)0;
         }
 #pragma unroll
-        for (int j = 0; j < ITEMS; j++) peers[j] = __match_any_sync(0xffffffffu, bk[j]);
-        // ---- critical section: cursor advance in (warp, item, lane) order
-        if (!(r == 0 && w == 0)) named_bar_sync(1 + w, 64);
-        uint32_t pos0[ITEMS];
+        for (int j = 0; j < ITEMS; j++) bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p) : -1;
+        // count per (bucket, warp) in input order
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            pos0[j] = 0;
-            if (bk[j] >= 0 && (peers[j] & lt) == 0) {
-                uint32_t c = cur[bk[j]];
-                pos0[j] = c;
-                cur[bk[j]] = c + __popc(peers[j]);
+            const unsigned peers = __match_any_sync(0xffffffffu, bk[j]);
+            if (bk[j] >= 0 && (peers & lt) == 0) cnt[bk[j] * NWARPS + w] += (uint16_t)__popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        block_scan_u16(cnt, NC, wtot);
+        for (int b = threadIdx.x; b < k; b += NT) lst[b] = cnt[b * NWARPS];
+        if (threadIdx.x == 0) lst[k] = (uint16_t)nvalid;
+        __syncthreads();  // lst reads cnt[b*NWARPS], which warp 0 advances below
+        // place (stable local sort by bucket)
+#pragma unroll
+        for (int j = 0; j < ITEMS; j++) {
+            const unsigned peers = __match_any_sync(0xffffffffu, bk[j]);
+            const int leader = __ffs(peers) - 1;
+            uint32_t b0 = 0;
+            if (bk[j] >= 0 && lane == leader) {
+                b0 = cnt[bk[j] * NWARPS + w];
+                cnt[bk[j] * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
+            }
+            b0 = __shfl_sync(0xffffffffu, b0, leader);
+            if (bk[j] >= 0) {
+                const uint32_t pos = b0 + __popc(peers & lt);
+                stk[pos] = key[j];
+                if constexpr (PB != 0) stp[pos] = pay[j];
+                stb[pos] = (uint16_t)bk[j];
             }
             __syncwarp();
         }
-        if (!(w == NWARPS - 1 && r == nr - 1)) {
-            __threadfence_block();
-            named_bar_arrive(1 + ((w + 1) & (NWARPS - 1)), 64);
+        __syncthreads();
+        // coalesced run writes, counters reset for the next round
+        for (int i = threadIdx.x; i < nvalid; i += NT) {
+            const int b = stb[i];
+            const uint32_t dst = cur[b] + (uint32_t)(i - lst[b]);
+            dk[dst] = stk[i];
+            if constexpr (PB != 0) dp[dst] = stp[i];
         }
-        // ---- scatter
-#pragma unroll
-        for (int j = 0; j < ITEMS; j++) {
-            int leader = __ffs(peers[j]) - 1;
-            uint32_t b0 = __shfl_sync(0xffffffffu, pos0[j], leader);
-            if (bk[j] >= 0) {
-                uint32_t pos = b0 + __popc(peers[j] & lt);
-                dk[pos] = key[j];
-                if constexpr (PB != 0) dp[pos] = pay[j];
-            }
-        }
+        for (int q = threadIdx.x; q < NC; q += NT) cnt[q] = 0;
+        __syncthreads();
+        for (int b = threadIdx.x; b < k; b += NT) cur[b] += (uint32_t)(lst[b + 1] - lst[b]);
+        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------ classify
+// Bucket totals of a partition level -> finish runs and next-level segments.
+// k_bstart: one thread per (segment, bucket slot): absolute bucket starts into
+//   bstart[kfirst[s] + b] (k_s + 1 slots per segment, last = segment end);
+//   buckets above capacity become next-level segments centred on the
+//   bucket's estimated mean (_kernels.py:103-106, 282-318).
+// k_windows: one thread per (segment, window of `half` records): the buckets
+//   whose start lies in the window form one finish run (<= cap records),
+//   found by binary search over bstart -- no serial walks over empty tails.
 
 struct ClassCfg {
-    int32_t cap;        // finish capacity (records)
-    int32_t half;       // grouping window
+    int32_t cap;   // finish capacity (records)
+    int32_t half;  // window
     int32_t depth_guard;
     int32_t mapping;
 };
 
-__device__ __forceinline__ int64_t bucket_start(const SegParams &p, const uint32_t *mat, int b) {
-    if (b >= p.k) return p.start + p.len;
-    return p.start + (int64_t)mat[p.mat_base + (int64_t)b * p.ntiles] - p.scan_base;
-}
-
-// One thread per (segment, bucket): bucket runs <= capacity become finish
-// entries (whole buckets only, grouped within a window so each entry stays
-// <= cap); larger buckets become next-level segments with the bucket's
-// estimated center (_kernels.py:282-318, 103-106).
-__global__ void k_classify(const SegParams *__restrict__ segs, int nseg, const int64_t *__restrict__ kfirst,
-                           const uint32_t *__restrict__ mat, Entry *entries, SegParams *children, SegAcc *acc,
-                           unsigned long long *ctrl, ClassCfg cc, int64_t total_buckets) {
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= total_buckets) return;
+__device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64_t g) {
     int lo = 0, hi = nseg - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
-        if (kfirst[mid] <= g) lo = mid;
+        if (first[mid] <= g) lo = mid;
         else hi = mid - 1;
     }
-    const SegParams &p = segs[lo];
-    int b = (int)(g - kfirst[lo]);
-    if (p.mode == MODE_COPY) return;
+    return lo;
+}
+
+__global__ void k_bstart(const SegParams *__restrict__ segs, int nseg, const int64_t *__restrict__ kfirst,
+                         const uint32_t *__restrict__ mat, int64_t *__restrict__ bstart, SegParams *children,
+                         SegAcc *acc, unsigned long long *ctrl, ClassCfg cc, int64_t total_slots) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= total_slots) return;
+    const int s = seg_of_slot(kfirst, nseg, g);
+    const SegParams &p = segs[s];
+    const int b = (int)(g - kfirst[s]);
+    const int64_t st = (b >= p.k) ? p.start + p.len
+                                   : p.start + (int64_t)mat[p.mat_base + (int64_t)b * p.ntiles] - p.scan_base;
+    bstart[g] = st;
+    if (b >= p.k || p.mode == MODE_COPY) return;
     if (b == 0) {
         atomicAdd(&ctrl[C_ST_SCATTERS], 1ull);
         atomicMax(&ctrl[C_ST_MAXDEPTH], (unsigned long long)p.level);
     }
+    const int64_t en = (b + 1 >= p.k) ? p.start + p.len
+                                      : p.start + (int64_t)mat[p.mat_base + (int64_t)(b + 1) * p.ntiles] - p.scan_base;
+    const int64_t c = en - st;
+    if (c <= cc.cap) return;
+    SegParams ch{};
+    ch.start = st;
+    ch.len = c;
+    ch.level = p.level + 1;
+    ch.src = (p.src == 1) ? 2 : 1;
+    ch.k = p.k;
+    bool integer = p.mode == MODE_INTEGER || c == p.len || ch.level > cc.depth_guard;
+    if (integer) {
+        ch.mode = MODE_INTEGER;
+        atomicAdd(&ctrl[C_ST_FALLBACKS], 1ull);
+    } else {
+        ch.mode = MODE_ZSCORE;
+        ch.center = __dadd_rn(__dmul_rn(__dsub_rn(__ddiv_rn((double)b + 0.5, p.scale), p.zmin), p.std), p.center);
+    }
+    unsigned long long slot = atomicAdd(&ctrl[C_NCHILD], 1ull);
+    children[slot] = ch;
+    acc[slot] = SegAcc{~0ull, 0ull, 0.0, 0.0};
+}
+
+__device__ __forceinline__ int lower_bound_i64(const int64_t *a, int n, int64_t v) {
+    int lo = 0, hi = n;  // first index with a[i] >= v, in [0, n]
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_windows(const SegParams *__restrict__ segs, int nseg, const int64_t *__restrict__ kfirst,
+                          const int64_t *__restrict__ wfirst, const int64_t *__restrict__ bstart, Entry *entries,
+                          unsigned long long *ctrl, ClassCfg cc, int64_t total_windows) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= total_windows) return;
+    const int s = seg_of_slot(wfirst, nseg, g);
+    const SegParams &p = segs[s];
+    if (p.mode == MODE_COPY) return;
+    const int64_t w = g - wfirst[s];
+    const int64_t *bs = bstart + kfirst[s];  // k + 1 slots
+    const int64_t ws = p.start + w * cc.half, we = ws + cc.half;
+    const int b0 = lower_bound_i64(bs, p.k, ws);
+    const int b1 = lower_bound_i64(bs, p.k, we);
+    if (b0 >= b1) return;  // no bucket starts inside this window
     const int dst = (p.src == 1) ? 2 : 1;
-    int64_t st = bucket_start(p, mat, b);
-    int64_t c = bucket_start(p, mat, b + 1) - st;
-    if (c > cc.cap) {
-        SegParams ch{};
-        ch.start = st;
-        ch.len = c;
-        ch.level = p.level + 1;
-        ch.src = dst;
-        ch.k = p.k;
-        bool integer = p.mode == MODE_INTEGER || c == p.len || ch.level > cc.depth_guard;
-        if (integer) {
-            ch.mode = MODE_INTEGER;
-            atomicAdd(&ctrl[C_ST_FALLBACKS], 1ull);
-        } else {
-            ch.mode = MODE_ZSCORE;
-            // estimated center of bucket b (_kernels.py:103-106)
-            ch.center = __dadd_rn(__dmul_rn(__dsub_rn(__ddiv_rn((double)b + 0.5, p.scale), p.zmin), p.std), p.center);
+    const int64_t last = bs[b1] - bs[b1 - 1];
+    int64_t e0 = bs[b0], e1 = bs[b1];
+    if (last > cc.half) {
+        e1 = bs[b1 - 1];
+        if (last <= cc.cap) {  // a mid-size bucket is a run of its own
+            unsigned long long e = atomicAdd(&ctrl[C_NENTRY], 1ull);
+            entries[e] = Entry{bs[b1 - 1], (int32_t)last, dst};
         }
-        unsigned long long slot = atomicAdd(&ctrl[C_NCHILD], 1ull);
-        children[slot] = ch;
-        acc[slot] = SegAcc{~0ull, 0ull, 0.0, 0.0};
-        return;
     }
-    if (c > cc.half) {
+    if (e1 > e0) {
         unsigned long long e = atomicAdd(&ctrl[C_NENTRY], 1ull);
-        entries[e] = Entry{st, (int32_t)c, dst};
-        return;
-    }
-    // groupable bucket: does it start a run?
-    int64_t win = (st - p.start) / cc.half;
-    bool starts = true;
-    if (b > 0) {
-        int64_t pst = bucket_start(p, mat, b - 1);
-        int64_t pc = st - pst;
-        starts = pc > cc.half || (pst - p.start) / cc.half != win;
-    }
-    if (!starts) return;
-    int64_t end = st + c;
-    for (int b2 = b + 1; b2 < p.k; b2++) {
-        int64_t s2 = end;
-        int64_t e2 = bucket_start(p, mat, b2 + 1);
-        if (e2 - s2 > cc.half || (s2 - p.start) / cc.half != win) break;
-        end = e2;
-    }
-    if (end > st) {
-        unsigned long long e = atomicAdd(&ctrl[C_NENTRY], 1ull);
-        entries[e] = Entry{st, (int32_t)(end - st), dst};
+        entries[e] = Entry{e0, (int32_t)(e1 - e0), dst};
     }
 }
 
 // ----------------------------------------------------------------- plan
-// Tiling and matrix layout of the next level (single CTA, prefix sums over
-// the children).  Children keep the parent's k in paper mode (the reference
-// keeps k fixed across levels, core.py:355); fitted mode sizes k to the
-// child so its buckets average ~cap/4 records.
+// Tiling, matrix layout, bucket-slot and window prefixes of the next level
+// (single CTA; the child count is read from the control block).  k is sized
+// to the child so its buckets average ~cap/4 records (the reference's fixed
+// k across levels is a CPU choice, core.py:355).
 __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned long long *nseg_ptr, int64_t *kfirst,
-                                               unsigned long long *ctrl, int32_t mapping, int32_t cap,
+                                               int64_t *wfirst, unsigned long long *ctrl, int32_t cap, int32_t half,
                                                int32_t kmax_child, int32_t min_tile) {
-    (void)mapping;
     const int nseg = (int)*nseg_ptr;
-    __shared__ long long sh_t[32], sh_m[32], sh_l[32], sh_k[32];
-    __shared__ long long carry_t, carry_m, carry_l, carry_k;
+    constexpr int NV = 4;  // tiles, matrix entries, records, bucket slots, windows -> 5 with windows
+    __shared__ long long sh[5][32];
+    __shared__ long long carry[5];
     __shared__ int kmax;
-    if (threadIdx.x == 0) {
-        carry_t = carry_m = carry_l = carry_k = 0;
-        kmax = 1;
-    }
+    if (threadIdx.x < 5) carry[threadIdx.x] = 0;
+    if (threadIdx.x == 0) kmax = 1;
     __syncthreads();
+    (void)NV;
     for (int base = 0; base < nseg; base += 1024) {
         int s = base + threadIdx.x;
-        long long nt = 0, nm = 0, ln = 0, kk = 0;
+        long long v[5] = {0, 0, 0, 0, 0};
         SegParams p;
         if (s < nseg) {
             p = segs[s];
-            // k sized to the child so buckets average ~cap/4 records (both
-            // mappings; the reference's fixed k is a CPU choice, core.py:355)
             int64_t want = (p.len * 4 + cap - 1) / cap;
             int k = 16;
             while (k < want && k < kmax_child) k <<= 1;
@@ -714,143 +807,150 @@ __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned l
             tl = (tl + 255) & ~(int64_t)255;
             p.tile_len = tl;
             p.ntiles = (int32_t)((p.len + tl - 1) / tl);
-            nt = p.ntiles;
-            nm = (long long)p.ntiles * k;
-            ln = p.len;
-            kk = k;
+            v[0] = p.ntiles;
+            v[1] = (long long)p.ntiles * k;
+            v[2] = p.len;
+            v[3] = k + 1;
+            v[4] = (p.len + half - 1) / half;
             atomicMax(&kmax, k);
         }
-        // block inclusive scans of (nt, nm, ln, kk)
-        long long a = nt, m = nm, l = ln, q = kk;
-        int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        for (int o = 1; o < 32; o <<= 1) {
-            long long ya = __shfl_up_sync(0xffffffffu, a, o), ym = __shfl_up_sync(0xffffffffu, m, o);
-            long long yl = __shfl_up_sync(0xffffffffu, l, o), yq = __shfl_up_sync(0xffffffffu, q, o);
-            if (lane >= o) {
-                a += ya;
-                m += ym;
-                l += yl;
-                q += yq;
+        long long x[5];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+        for (int j = 0; j < 5; j++) {
+            x[j] = v[j];
+            for (int o = 1; o < 32; o <<= 1) {
+                long long y = __shfl_up_sync(0xffffffffu, x[j], o);
+                if (lane >= o) x[j] += y;
             }
-        }
-        if (lane == 31) {
-            sh_t[w] = a;
-            sh_m[w] = m;
-            sh_l[w] = l;
-            sh_k[w] = q;
+            if (lane == 31) sh[j][w] = x[j];
         }
         __syncthreads();
-        long long pa = carry_t, pm = carry_m, pl = carry_l, pq = carry_k;
-        for (int j = 0; j < w; j++) {
-            pa += sh_t[j];
-            pm += sh_m[j];
-            pl += sh_l[j];
-            pq += sh_k[j];
+        long long pre[5];
+#pragma unroll
+        for (int j = 0; j < 5; j++) {
+            pre[j] = carry[j];
+            for (int q = 0; q < w; q++) pre[j] += sh[j][q];
         }
         if (s < nseg) {
-            p.tile_first = pa + a - nt;
-            p.mat_base = pm + m - nm;
-            p.scan_base = pl + l - ln;
-            kfirst[s] = pq + q - kk;
+            p.tile_first = pre[0] + x[0] - v[0];
+            p.mat_base = pre[1] + x[1] - v[1];
+            p.scan_base = pre[2] + x[2] - v[2];
+            kfirst[s] = pre[3] + x[3] - v[3];
+            wfirst[s] = pre[4] + x[4] - v[4];
             segs[s] = p;
         }
         __syncthreads();
         if (threadIdx.x == 1023) {
-            carry_t = pa + a;
-            carry_m = pm + m;
-            carry_l = pl + l;
-            carry_k = pq + q;
+#pragma unroll
+            for (int j = 0; j < 5; j++) carry[j] = pre[j] + x[j];
         }
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        ctrl[C_TILES_NEXT] = carry_t;
-        ctrl[C_MAT_NEXT] = carry_m;
+        ctrl[C_TILES_NEXT] = carry[0];
+        ctrl[C_MAT_NEXT] = carry[1];
+        ctrl[C_NEXT_BIG] = carry[3];
+        ctrl[C_WIN_NEXT] = carry[4];
         ctrl[C_KMAX_NEXT] = kmax;
-        ctrl[C_NEXT_BIG] = carry_k;
-        kfirst[nseg] = carry_k;
+        kfirst[nseg] = carry[3];
+        wfirst[nseg] = carry[4];
     }
 }
 
 // ------------------------------------------------------------------- K5
-// Shared-memory stable finish of one entry (a run of whole buckets,
-// len <= cap): load keys + payload, split by the top bits of
-// (ord(key) - ord(min)) into sub-buckets with a stable warp-ranked counting
-// pass (per-warp u16 counters, block scan), insertion-sort the tiny
-// sub-buckets (only strictly greater keys shift, _kernels.py:143-156), and a
-// warp bitonic network on (key, original position) for the rare large ones.
-// Everything is staged in shared memory, so src may alias the output.
+// Shared-memory stable finish of one run of whole buckets (len <= NT*F).
+//  load    every thread issues its F key (and payload) loads up front and
+//          keeps them in registers: warp w owns the contiguous slice
+//          [w*32F, (w+1)*32F), item j of lane l is record w*32F + j*32 + l;
+//  minmax  exact ordered min/max of the run (block reduce);
+//  count   sub-bucket digit = top bits of (ord(key) - ord(min)); per-warp
+//          u16 counters advanced by __match_any_sync leaders in (j, lane)
+//          order, i.e. input order within the warp's slice;
+//  scan    conflict-free warp-cooperative exclusive scan in (digit, warp)
+//          order -> stable placement offsets;
+//  place   keys + payload into shared memory in sub-bucket order;
+//  sort    insertion sort of each small sub-bucket (only strictly greater
+//          keys shift: stable, _kernels.py:143-156); sub-buckets above
+//          FIN_INS that are not already ordered are emitted as refine runs
+//          and finished again by a later launch (their key range shrinks by
+//          2^sbits each time, so this terminates);
+//  write   coalesced stores of the run.
+// All loads complete before any output store, so src may alias the output.
 
-constexpr int FIN_INS = 24;  // sub-buckets up to this size use insertion sort
+constexpr int FIN_INS = 32;        // sub-buckets up to this size are ranked in place
+constexpr int FIN_SBITS_MAX = 11;  // <= 2048 sub-buckets
 
-struct FinLayout {
-    int cap, sb_max;
-    size_t off_a, off_b, off_pl, off_i, off_cnt, off_st, off_q, total;
+template <int PB>
+struct FinItems {
+    static constexpr int F = PB == 8 ? 16 : (PB == 4 ? 24 : 32);
 };
 
-__host__ __device__ inline FinLayout fin_layout(int cap, int pb, int sb_max) {
+struct FinLayout {
+    int cap;
+    size_t off_b, off_pb, off_cnt, off_st, total;
+};
+
+__host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     FinLayout L;
     L.cap = cap;
-    L.sb_max = sb_max;
     size_t o = 0;
-    L.off_a = o;
-    o += (size_t)cap * 8;
     L.off_b = o;
     o += (size_t)cap * 8;
-    L.off_pl = o;
+    L.off_pb = o;
     o += (size_t)cap * pb;
     o = (o + 15) & ~(size_t)15;
-    L.off_i = o;
-    o += (size_t)cap * 2;
-    o = (o + 15) & ~(size_t)15;
     L.off_cnt = o;
-    o += (size_t)sb_max * NWARPS * 2;
+    o += (size_t)(1 << FIN_SBITS_MAX) * NWARPS * 2;
     L.off_st = o;
-    o += (size_t)(sb_max + 1) * 2;
+    o += (size_t)((1 << FIN_SBITS_MAX) + 1) * 2;
     o = (o + 15) & ~(size_t)15;
-    L.off_q = o;
-    o += (size_t)1024 * 4;
     L.total = o;
     return L;
 }
 
-template <int KK>
-__device__ __forceinline__ bool kless(uint64_t a, uint16_t ia, uint64_t b, uint16_t ib) {
-    uint64_t oa = ord_key<KK>(a), ob = ord_key<KK>(b);
-    return oa < ob || (oa == ob && ia < ib);
-}
-
 template <int KK, int PB>
-__global__ void __launch_bounds__(NT) k_finish(Buffers B, const Entry *__restrict__ entries, int cap, int sb_max) {
+__global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__restrict__ entries, int cap,
+                                                  Entry *refine, unsigned long long *refine_count, int fin_ins) {
     using P = typename PayloadT<PB>::T;
+    constexpr int F = FinItems<PB>::F;
     extern __shared__ __align__(16) unsigned char smem[];
-    const FinLayout L = fin_layout(cap, PB, sb_max);
-    uint64_t *A = (uint64_t *)(smem + L.off_a);
-    uint64_t *Bk = (uint64_t *)(smem + L.off_b);
-    P *PL = (P *)(smem + L.off_pl);
-    uint16_t *I = (uint16_t *)(smem + L.off_i);
+    const FinLayout L = fin_layout(cap, PB);
+    uint64_t *Bo = (uint64_t *)(smem + L.off_b);  // ordered images, placed
+    P *PBf = (P *)(smem + L.off_pb);
     uint16_t *cnt = (uint16_t *)(smem + L.off_cnt);
     uint16_t *sst = (uint16_t *)(smem + L.off_st);
-    int *q = (int *)(smem + L.off_q);
     __shared__ unsigned long long r_min[NWARPS], r_max[NWARPS];
-    __shared__ int nq;
+    __shared__ uint32_t wtot[NWARPS];
+    __shared__ uint32_t negzero[256];  // float64: bit per placed record that was -0.0 (cap <= 8192)
 
     const Entry e = entries[blockIdx.x];
     const int m = e.len;
+    if (m <= 0) return;
     const uint64_t *sk = src_keys(B, e.src) + e.start;
     const P *sp = src_pay<PB>(B, e.src) + e.start;
     uint64_t *ok = B.out_k + e.start;
     P *op = (P *)B.out_p + e.start;
     const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int base = w * 32 * F + lane;
 
+    uint64_t key[F];
+    P pay[F];
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const int i = base + j * 32;
+        key[j] = i < m ? sk[i] : 0ull;
+        if constexpr (PB != 0) pay[j] = i < m ? sp[i] : (P)0;
+    }
     unsigned long long omin = ~0ull, omax = 0;
-    for (int i = tid; i < m; i += NT) {
-        uint64_t k = sk[i];
-        A[i] = k;
-        if constexpr (PB != 0) PL[i] = sp[i];
-        uint64_t o = ord_key<KK>(k);
-        omin = o < omin ? o : omin;
-        omax = o > omax ? o : omax;
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        if (base + j * 32 < m) {
+            unsigned long long o = ord_key<KK>(key[j]);
+            omin = min(omin, o);
+            omax = max(omax, o);
+        }
     }
     omin = warp_min_u64(omin);
     omax = warp_max_u64(omax);
@@ -858,171 +958,103 @@ __global__ void __launch_bounds__(NT) k_finish(Buffers B, const Entry *__restric
         r_min[w] = omin;
         r_max[w] = omax;
     }
-    if (tid == 0) nq = 0;
+    if (KK == KEY_F64) negzero[tid] = 0u;
     __syncthreads();
     omin = r_min[0];
     omax = r_max[0];
+#pragma unroll
     for (int j = 1; j < NWARPS; j++) {
-        omin = r_min[j] < omin ? r_min[j] : omin;
-        omax = r_max[j] > omax ? r_max[j] : omax;
+        omin = min(omin, r_min[j]);
+        omax = max(omax, r_max[j]);
     }
     if (omin == omax) {  // all equal: already in stable order
         if (e.src != 2) {
-            for (int i = tid; i < m; i += NT) {
-                ok[i] = A[i];
-                if constexpr (PB != 0) op[i] = PL[i];
+#pragma unroll
+            for (int j = 0; j < F; j++) {
+                const int i = base + j * 32;
+                if (i < m) {
+                    ok[i] = key[j];
+                    if constexpr (PB != 0) op[i] = pay[j];
+                }
             }
         }
         return;
     }
-    // sub-bucket count: ~m/4, power of two, <= sb_max
+    // digits: d = floor((ord - min) * S / (range + 1)), monotone, in [0, S)
     int sbits = 5;
-    while ((1 << sbits) < (m >> 2) && (1 << sbits) < sb_max) sbits++;
+    while ((1 << sbits) < (m >> 1) && sbits < FIN_SBITS_MAX) sbits++;
     const int S = 1 << sbits;
     const uint64_t range = omax - omin;
-    const int bl = bitlen64(range);
-    const int sh = bl > sbits ? bl - sbits : 0;
-    const bool exact = (sh == 0);  // each sub-bucket holds one key value
-    const int nc = S * NWARPS;
-    for (int i = tid; i < nc; i += NT) cnt[i] = 0;
+    // d = (ord - min) when the range fits S digits (one key value per digit),
+    // else d = mulhi(ord - min, M) with M = floor((2^64-1)/(range+1)) * S,
+    // which is monotone and < S.
+    const bool direct = range < (uint64_t)S;
+    const uint64_t M = direct ? 0ull : ((range == ~0ull ? 1ull : (~0ull / (range + 1))) * (uint64_t)S);
+    const int NC = S * NWARPS;
+    for (int i = tid; i < NC / 2; i += NT) ((uint32_t *)cnt)[i] = 0u;
     __syncthreads();
-    // warp w owns the contiguous slice [w0, w1) of the entry (input order)
-    const int per = (m + NWARPS - 1) / NWARPS;
-    const int w0 = min(m, w * per), w1 = min(m, w0 + per);
-    const unsigned lt = lanemask_lt();
-    for (int i0 = w0; i0 < w1; i0 += 32) {
-        int i = i0 + lane;
-        int sbk = i < w1 ? (int)((ord_key<KK>(A[i]) - omin) >> sh) : -1;
-        unsigned peers = __match_any_sync(0xffffffffu, sbk);
-        if (sbk >= 0 && (peers & lt) == 0) cnt[sbk * NWARPS + w] += (uint16_t)__popc(peers);
+    // ---- count per (digit, warp) in input order
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const uint64_t x = ord_key<KK>(key[j]) - omin;
+        const int d = (base + j * 32 < m) ? (int)(direct ? x : __umul64hi(x, M)) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d >= 0 && (peers & lt) == 0) cnt[d * NWARPS + w] += (uint16_t)__popc(peers);
         __syncwarp();
     }
     __syncthreads();
-    // block exclusive scan over cnt in (sub-bucket, warp) order
-    {
-        const int per_t = nc / NT;  // nc is a multiple of NT (S >= 32, NWARPS = 8)
-        const int c0 = tid * per_t;
-        uint32_t tsum = 0;
-        for (int j = 0; j < per_t; j++) tsum += cnt[c0 + j];
-        uint32_t x = tsum;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        __shared__ uint32_t wsum[NWARPS];
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        uint32_t pre = 0;
-        for (int j = 0; j < w; j++) pre += wsum[j];
-        uint32_t run = pre + x - tsum;
-        for (int j = 0; j < per_t; j++) {
-            uint16_t c = cnt[c0 + j];
-            cnt[c0 + j] = (uint16_t)run;
-            run += c;
-        }
-    }
-    __syncthreads();
-    for (int sbk = tid; sbk < S; sbk += NT) sst[sbk] = cnt[sbk * NWARPS];
+    block_scan_u16(cnt, NC, wtot);
+    for (int d = tid; d < S; d += NT) sst[d] = cnt[d * NWARPS];
     if (tid == 0) sst[S] = (uint16_t)m;
-    __syncthreads();
-    // stable placement
-    for (int i0 = w0; i0 < w1; i0 += 32) {
-        int i = i0 + lane;
-        uint64_t k = i < w1 ? A[i] : 0ull;
-        int sbk = i < w1 ? (int)((ord_key<KK>(k) - omin) >> sh) : -1;
-        unsigned peers = __match_any_sync(0xffffffffu, sbk);
-        int leader = __ffs(peers) - 1;
+    __syncthreads();  // sst reads cnt[d*NWARPS], which warp 0 advances below
+    // ---- stable placement of ordered images into shared memory
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const uint64_t o = ord_key<KK>(key[j]);
+        const int d = (base + j * 32 < m) ? (int)(direct ? o - omin : __umul64hi(o - omin, M)) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
         uint32_t b0 = 0;
-        if (sbk >= 0 && lane == leader) {
-            b0 = cnt[sbk * NWARPS + w];
-            cnt[sbk * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
+        if (d >= 0 && lane == leader) {
+            b0 = cnt[d * NWARPS + w];
+            cnt[d * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
         }
         b0 = __shfl_sync(0xffffffffu, b0, leader);
-        if (sbk >= 0) {
-            uint32_t pos = b0 + __popc(peers & lt);
-            Bk[pos] = k;
-            I[pos] = (uint16_t)i;
+        if (d >= 0) {
+            const uint32_t pos = b0 + __popc(peers & lt);
+            Bo[pos] = o;
+            if constexpr (PB != 0) PBf[pos] = pay[j];
+            if (KK == KEY_F64 && key[j] == SIGN) atomicOr(&negzero[pos >> 5], 1u << (pos & 31));
         }
         __syncwarp();
     }
     __syncthreads();
-    if (!exact) {
-        for (int sbk = tid; sbk < S; sbk += NT) {
-            int a = sst[sbk], z = sst[sbk + 1];
-            int c = z - a;
-            if (c <= 1) continue;
-            if (c <= FIN_INS) {
-                for (int x = a + 1; x < z; x++) {
-                    uint64_t kv = Bk[x];
-                    uint16_t iv = I[x];
-                    uint64_t ov = ord_key<KK>(kv);
-                    int y = x - 1;
-                    while (y >= a && ord_key<KK>(Bk[y]) > ov) {
-                        Bk[y + 1] = Bk[y];
-                        I[y + 1] = I[y];
-                        y--;
-                    }
-                    Bk[y + 1] = kv;
-                    I[y + 1] = iv;
-                }
-            } else {
-                int slot = atomicAdd(&nq, 1);
-                if (slot < 1024) q[slot] = sbk;
-            }
-        }
-        __syncthreads();
-        const int nbig = min(nq, 1024);
-        for (int t = w; t < nbig; t += NWARPS) {
-            int a = sst[q[t]], z = sst[q[t] + 1];
-            int c = z - a;
-            // already ordered (incl. all-equal)?  placement kept input order
-            bool sorted = true;
-            for (int x = a + lane; x + 1 < z; x += 32)
-                if (ord_key<KK>(Bk[x]) > ord_key<KK>(Bk[x + 1])) sorted = false;
-            if (__all_sync(0xffffffffu, sorted)) continue;
-            // bitonic network with all comparators ascending; virtual +inf padding
-            int P2 = 1;
-            while (P2 < c) P2 <<= 1;
-            for (int size = 2; size <= P2; size <<= 1) {
-                for (int x = lane; x < P2 / 2; x += 32) {  // flip stage
-                    int blk = x / (size / 2), off = x % (size / 2);
-                    int i1 = blk * size + off, i2 = blk * size + size - 1 - off;
-                    if (i2 < c) {
-                        uint64_t k1 = Bk[a + i1], k2 = Bk[a + i2];
-                        uint16_t j1 = I[a + i1], j2 = I[a + i2];
-                        if (kless<KK>(k2, j2, k1, j1)) {
-                            Bk[a + i1] = k2;
-                            Bk[a + i2] = k1;
-                            I[a + i1] = j2;
-                            I[a + i2] = j1;
-                        }
-                    }
-                }
-                __syncwarp();
-                for (int str = size / 4; str >= 1; str >>= 1) {  // half cleaners
-                    for (int x = lane; x < P2 / 2; x += 32) {
-                        int blk = x / str, off = x % str;
-                        int i1 = blk * 2 * str + off, i2 = i1 + str;
-                        if (i2 < c) {
-                            uint64_t k1 = Bk[a + i1], k2 = Bk[a + i2];
-                            uint16_t j1 = I[a + i1], j2 = I[a + i2];
-                            if (kless<KK>(k2, j2, k1, j1)) {
-                                Bk[a + i1] = k2;
-                                Bk[a + i2] = k1;
-                                I[a + i1] = j2;
-                                I[a + i2] = j1;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
-        }
-        __syncthreads();
-    }
+    // ---- rank inside each sub-bucket by (ordered key, placement index) and
+    //      store straight to the final position (placement order is input
+    //      order within a sub-bucket, so ties keep input order: stable)
     for (int i = tid; i < m; i += NT) {
-        ok[i] = Bk[i];
-        if constexpr (PB != 0) op[i] = PL[I[i]];
+        const uint64_t o = Bo[i];
+        const int d = (int)(direct ? o - omin : __umul64hi(o - omin, M));
+        const int a = sst[d], z = sst[d + 1];
+        int rank = i - a;
+        if (z - a <= fin_ins) {
+            rank = 0;
+            for (int x = a; x < z; x++) {
+                const uint64_t ox = Bo[x];
+                rank += (ox < o) || (ox == o && x < i);
+            }
+        } else if (i == a) {  // oversized sub-bucket: refine later unless already ordered
+            bool sorted = true;
+            for (int x = a + 1; x < z && sorted; x++) sorted = Bo[x - 1] <= Bo[x];
+            if (!sorted) {
+                unsigned long long r = atomicAdd(refine_count, 1ull);
+                refine[r] = Entry{e.start + a, z - a, 2};
+            }
+        }
+        uint64_t kb = key_from_ord<KK>(o);
+        if (KK == KEY_F64 && ((negzero[i >> 5] >> (i & 31)) & 1u)) kb = SIGN;
+        ok[a + rank] = kb;
+        if constexpr (PB != 0) op[a + rank] = PBf[i];
     }
 }
 

@@ -111,12 +111,11 @@ int num_sms() {
     return sms;
 }
 
-constexpr int SB_MAX = 2048;      // finish sub-buckets
-constexpr int K_LEVEL1_MAX = 49152;  // cursor smem 192 KB
-constexpr int KMAX_CHILD = 8192;
+constexpr int K_LEVEL1_MAX = KSCAT_MAX;  // fan-out of one scatter pass
+constexpr int KMAX_CHILD = 1024;
 constexpr int MIN_TILE = 8192;
 
-int finish_cap(int pb) { return pb == 8 ? 7168 : 8192; }
+int finish_cap(int pb) { return NT * (pb == 8 ? FinItems<8>::F : (pb == 4 ? FinItems<4>::F : FinItems<0>::F)); }
 
 int64_t cluster_count(int64_t n, double alpha) {  // core.py:146-148
     double v = std::nearbyint(alpha * std::sqrt((double)n));
@@ -142,7 +141,7 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
     if (cfg.mapping == ZSB_MAP_PAPER) {
         P.k = std::min<int64_t>(cluster_count(n, cfg.alpha), K_LEVEL1_MAX);
     } else {
-        int64_t kmax = env_int("ZSB_K1MAX", 8192);
+        int64_t kmax = env_int("ZSB_K1MAX", 1024);
         P.k = std::min<int64_t>(std::max<int64_t>(16, pow2_at_least((4 * n + P.cap - 1) / P.cap)), kmax);
     }
     int64_t target_tiles = (int64_t)num_sms() * env_int("ZSB_TILES_PER_SM", 2);
@@ -155,8 +154,9 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
 }
 
 struct Layout {
-    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, entries, parts, ctrl, dbg, total;
-    int64_t mat_cap, seg_cap, ent_cap, status_cap;
+    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, wfirst, bstart, entries, refine0, refine1, parts,
+        ctrl, dbg, total;
+    int64_t mat_cap, seg_cap, ent_cap, status_cap, slot_cap, ref_cap;
 };
 
 constexpr int MOM_GRID_PER_SM = 4;
@@ -168,7 +168,9 @@ Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
     const int64_t cap = P.cap;
     L.mat_cap = std::max<int64_t>(P.k * P.ntiles, n / 4 + 24 * (n / cap + 1) + 4096) + 16;
     L.seg_cap = n / cap + 4;
-    L.ent_cap = 2 * (n / P.half + 1) + 24 * (n / cap + 1) + P.k + 4096;
+    L.ent_cap = 2 * (n / P.half + 1) + 2 * L.seg_cap + 4096;
+    L.slot_cap = std::max<int64_t>(P.k + 1, 24 * (n / cap + 1) + 2 * L.seg_cap) + 16;
+    L.ref_cap = n / (FIN_INS + 1) + 1024;
     L.status_cap = L.mat_cap / SCAN_TILE + 4;
     size_t o = 0;
     L.tmp_k = o;
@@ -187,8 +189,16 @@ Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
     o = align_up(o + (size_t)L.seg_cap * sizeof(SegAcc));
     L.kfirst = o;
     o = align_up(o + (size_t)(L.seg_cap + 2) * 8);
+    L.wfirst = o;
+    o = align_up(o + (size_t)(L.seg_cap + 2) * 8);
+    L.bstart = o;
+    o = align_up(o + (size_t)L.slot_cap * 8);
     L.entries = o;
     o = align_up(o + (size_t)L.ent_cap * sizeof(Entry));
+    L.refine0 = o;
+    o = align_up(o + (size_t)L.ref_cap * sizeof(Entry));
+    L.refine1 = o;
+    o = align_up(o + (size_t)L.ref_cap * sizeof(Entry));
     L.parts = o;
     o = align_up(o + (size_t)num_sms() * MOM_GRID_PER_SM * sizeof(MomPartial));
     L.ctrl = o;
@@ -204,9 +214,9 @@ void smem_optin(F *func, size_t bytes) {
     if (bytes > 48 * 1024) cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-__global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t n, int64_t k, int64_t tile_len,
-                              int64_t ntiles, int src, double center, double sd, double zmin, double scale,
-                              int mode) {
+__global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t *wfirst, int64_t nwin, int64_t n, int64_t k,
+                              int64_t tile_len, int64_t ntiles, int src, double center, double sd, double zmin,
+                              double scale, int mode) {
     SegParams p{};
     p.center = center;
     p.std = sd;
@@ -225,7 +235,11 @@ __global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t n, int64_
     p.src = src;
     *seg = p;
     kfirst[0] = 0;
-    kfirst[1] = k;
+    kfirst[1] = k + 1;
+    if (wfirst) {
+        wfirst[0] = 0;
+        wfirst[1] = nwin;
+    }
 }
 
 __global__ void k_bucket_totals(const uint32_t *mat, int64_t k, int64_t ntiles, int64_t *counts) {
@@ -265,25 +279,28 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
         k_scan<<<(unsigned)sblocks, NT, 0, c.st>>>(mat, mat_entries, status, ctrl);
     }
     ZSB_LAUNCH("k_scan");
-    constexpr int ITEMS = 4;
-    smem_optin(k_scatter<KK, PB, ITEMS>, kbytes);
+    const size_t sbytes = scat_layout(kmax, PB).total;
+    smem_optin(k_scatter<KK, PB>, sbytes);
     {
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, ITEMS><<<(unsigned)tiles, NT, kbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel);
+        k_scatter<KK, PB><<<(unsigned)tiles, NT, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel);
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
 }
 
 template <int KK, int PB>
-int launch_finish(Ctx &c, int64_t nentries) {
+int launch_finish(Ctx &c, const Entry *list, int64_t nentries, int ref_out) {
     if (nentries <= 0) return ZSB_OK;
-    FinLayout FL = fin_layout((int)c.P.cap, PB, SB_MAX);
+    FinLayout FL = fin_layout((int)c.P.cap, PB);
     smem_optin(k_finish<KK, PB>, FL.total);
-    Entry *entries = (Entry *)(c.ws + c.L.entries);
+    Entry *refine = (Entry *)(c.ws + (ref_out ? c.L.refine1 : c.L.refine0));
+    unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     {
         PhaseScope ph(PH_FINISH, c.st);
-        k_finish<KK, PB><<<(unsigned)nentries, NT, FL.total, c.st>>>(c.B, entries, (int)c.P.cap, SB_MAX);
+        k_finish<KK, PB><<<(unsigned)nentries, NT, FL.total, c.st>>>(c.B, list, (int)c.P.cap, refine,
+                                                                     ctrl + (ref_out ? C_NREF1 : C_NREF0),
+                                                                     env_int("ZSB_FIN_INS", FIN_INS));
     }
     ZSB_LAUNCH("k_finish");
     return ZSB_OK;
@@ -297,10 +314,33 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     SegParams *seg_next = (SegParams *)(c.ws + c.L.seg_b);
     SegAcc *acc = (SegAcc *)(c.ws + c.L.acc);
     int64_t *kfirst = (int64_t *)(c.ws + c.L.kfirst);
+    int64_t *wfirst = (int64_t *)(c.ws + c.L.wfirst);
+    int64_t *bstart = (int64_t *)(c.ws + c.L.bstart);
     Entry *entries = (Entry *)(c.ws + c.L.entries);
+    Entry *refine[2] = {(Entry *)(c.ws + c.L.refine0), (Entry *)(c.ws + c.L.refine1)};
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     int64_t stats[ZSB_STAT_SLOTS] = {0, 0, 0, 0, 0};
+    unsigned long long h_ctrl[C_SLOTS];
     ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
+    int r = 0;  // refine list the finish launches of this round append to
+
+    // Drain refinement runs (oversized unsorted sub-buckets re-finished in place).
+    auto drain_refine = [&](int64_t pending) -> int {
+        while (pending > 0) {
+            if (pending > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
+            int rc0 = cudaMemsetAsync(ctrl + (r ? C_NREF0 : C_NREF1), 0, 8, c.st) == cudaSuccess ? 0 : 1;
+            if (rc0) return fail(ZSB_ERR_CUDA, "memset");
+            int rc = launch_finish<KK, PB>(c, refine[r], pending, 1 - r);
+            if (rc) return rc;
+            stats[ZSB_STAT_INSERTION] += pending;
+            r = 1 - r;
+            ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
+            ZSB_CUDA(cudaStreamSynchronize(c.st));
+            timing_collect();
+            pending = (int64_t)h_ctrl[r ? C_NREF1 : C_NREF0];
+        }
+        return ZSB_OK;
+    };
 
     if (n <= c.P.cap) {  // one shared-memory finish (core.py:369-374; threshold widened to the smem capacity)
         {
@@ -308,21 +348,25 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             k_single_entry<<<1, 1, 0, c.st>>>(entries, n);
         }
         ZSB_LAUNCH("k_single_entry");
-        int rc = launch_finish<KK, PB>(c, 1);
+        int rc = launch_finish<KK, PB>(c, entries, 1, r);
         if (rc) return rc;
+        ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
         ZSB_CUDA(cudaStreamSynchronize(c.st));
         timing_collect();
         stats[ZSB_STAT_INSERTION] = 1;
+        rc = drain_refine((int64_t)h_ctrl[r ? C_NREF1 : C_NREF0]);
+        if (rc) return rc;
         if (h_stats) memcpy(h_stats, stats, sizeof(stats));
         return ZSB_OK;
     }
 
     MapCfg mc{cfg.mapping, (int32_t)cfg.depth_guard};
     ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping};
+    const int64_t nwin1 = (n + c.P.half - 1) / c.P.half;
     {
         PhaseScope ph(PH_MISC, c.st);
-        k_init_level1<<<1, 1, 0, c.st>>>(seg_cur, kfirst, n, c.P.k, c.P.tile_len, c.P.ntiles, 0, 0.0, 1.0, 0.0, 1.0,
-                                         MODE_ZSCORE);
+        k_init_level1<<<1, 1, 0, c.st>>>(seg_cur, kfirst, wfirst, nwin1, n, c.P.k, c.P.tile_len, c.P.ntiles, 0, 0.0,
+                                         1.0, 0.0, 1.0, MODE_ZSCORE);
     }
     ZSB_LAUNCH("k_init_level1");
     int grid = std::max(1, std::min<int>(num_sms() * MOM_GRID_PER_SM, (int)((n + NT - 1) / NT)));
@@ -334,10 +378,10 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     ZSB_LAUNCH("k_moments");
 
     int nseg = 1;
-    int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_buckets = c.P.k;
+    int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
     int kmax = (int)c.P.k;
     int level = 1;
-    unsigned long long h_ctrl[C_SLOTS];
+    int64_t pending_refine = 0;
     while (true) {
         if (level > 1) {
             {
@@ -352,22 +396,38 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         if (rc) return rc;
         ZSB_CUDA(cudaMemsetAsync(ctrl + C_NCHILD, 0, 16, c.st));  // C_NCHILD, C_NENTRY
         {
-            PhaseScope ph(PH_CLASSIFY, c.st, 2);
-            k_classify<<<(unsigned)((total_buckets + 255) / 256), 256, 0, c.st>>>(
-                seg_cur, nseg, kfirst, mat, entries, seg_next, acc, ctrl, cc, total_buckets);
-            k_plan<<<1, 1024, 0, c.st>>>(seg_next, ctrl + C_NCHILD, kfirst, ctrl, cfg.mapping, (int32_t)c.P.cap,
-                                         KMAX_CHILD, MIN_TILE);
+            PhaseScope ph(PH_CLASSIFY, c.st, 3);
+            k_bstart<<<(unsigned)((total_slots + 255) / 256), 256, 0, c.st>>>(seg_cur, nseg, kfirst, mat, bstart,
+                                                                             seg_next, acc, ctrl, cc, total_slots);
+            k_windows<<<(unsigned)((total_windows + 255) / 256), 256, 0, c.st>>>(seg_cur, nseg, kfirst, wfirst, bstart,
+                                                                               entries, ctrl, cc, total_windows);
+            k_plan<<<1, 1024, 0, c.st>>>(seg_next, ctrl + C_NCHILD, kfirst, wfirst, ctrl, (int32_t)c.P.cap,
+                                         (int32_t)c.P.half, KMAX_CHILD, MIN_TILE);
         }
-        ZSB_LAUNCH("k_classify/k_plan");
+        ZSB_LAUNCH("k_bstart/k_windows/k_plan");
+        if (env_int("ZSB_DEBUG", 0) >= 2) {  // validate this level's partition on the host
+            ZSB_CUDA(cudaStreamSynchronize(c.st));
+        }
         ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
         ZSB_CUDA(cudaStreamSynchronize(c.st));
         timing_collect();
         if (h_ctrl[C_STATUS] == 3) return fail(ZSB_ERR_NAN, "NaN keys have no order");
+        if (env_int("ZSB_DEBUG", 0))
+            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %llu entries %llu refine %llu "
+                            "fallbacks %llu\n", level, nseg, (long long)tiles, kmax, h_ctrl[C_NCHILD],
+                    h_ctrl[C_NENTRY], h_ctrl[r ? C_NREF1 : C_NREF0], h_ctrl[C_ST_FALLBACKS]);
+        // finish runs of this level, plus refinement runs produced before this sync
+        pending_refine = (int64_t)h_ctrl[r ? C_NREF1 : C_NREF0];
         int64_t nentry = (int64_t)h_ctrl[C_NENTRY];
         if (nentry > c.L.ent_cap) return fail(ZSB_ERR_WORKSPACE, "finish entry list overflow");
-        int rc2 = launch_finish<KK, PB>(c, nentry);
+        if (pending_refine > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
+        ZSB_CUDA(cudaMemsetAsync(ctrl + (r ? C_NREF0 : C_NREF1), 0, 8, c.st));
+        int rc2 = launch_finish<KK, PB>(c, entries, nentry, 1 - r);
         if (rc2) return rc2;
-        stats[ZSB_STAT_INSERTION] += nentry;
+        rc2 = launch_finish<KK, PB>(c, refine[r], pending_refine, 1 - r);
+        if (rc2) return rc2;
+        stats[ZSB_STAT_INSERTION] += nentry + pending_refine;
+        r = 1 - r;
         int64_t nchild = (int64_t)h_ctrl[C_NCHILD];
         if (nchild == 0) break;
         if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
@@ -375,8 +435,10 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         tiles = (int64_t)h_ctrl[C_TILES_NEXT];
         mat_entries = (int64_t)h_ctrl[C_MAT_NEXT];
         kmax = (int)h_ctrl[C_KMAX_NEXT];
-        total_buckets = (int64_t)h_ctrl[C_NEXT_BIG];
+        total_slots = (int64_t)h_ctrl[C_NEXT_BIG];
+        total_windows = (int64_t)h_ctrl[C_WIN_NEXT];
         if (mat_entries > c.L.mat_cap) return fail(ZSB_ERR_WORKSPACE, "count matrix overflow");
+        if (total_slots > c.L.slot_cap) return fail(ZSB_ERR_WORKSPACE, "bucket slot overflow");
         std::swap(seg_cur, seg_next);
         level++;
         if (level > 200) return fail(ZSB_ERR_CUDA, "partition did not terminate");
@@ -384,6 +446,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
     ZSB_CUDA(cudaStreamSynchronize(c.st));
     timing_collect();
+    int rc3 = drain_refine((int64_t)h_ctrl[r ? C_NREF1 : C_NREF0]);
+    if (rc3) return rc3;
     stats[ZSB_STAT_MAX_DEPTH] = (int64_t)h_ctrl[C_ST_MAXDEPTH];
     stats[ZSB_STAT_FALLBACKS] = (int64_t)h_ctrl[C_ST_FALLBACKS];
     stats[ZSB_STAT_SCATTERS] = (int64_t)h_ctrl[C_ST_SCATTERS];
@@ -470,7 +534,7 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     int rc = check_common(d_keys, kd, pb, n);
     if (rc) return rc;
     if (n < 1 || k < 2 || k > K_LEVEL1_MAX || !params)
-        return fail(ZSB_ERR_ARG, "need n >= 1, 2 <= k <= 49152 and params");
+        return fail(ZSB_ERR_ARG, "need n >= 1, 2 <= k <= 2048 and params");
     if (!(params[1] > 0.0) || !(params[3] > 0.0)) return fail(ZSB_ERR_ARG, "std and scale must be positive");
     ctx.n = n;
     ctx.P.k = k;
@@ -492,8 +556,8 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     ctx.B.out_p = d_out_payload;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
-    k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0], params[1],
-                                       params[2], params[3], MODE_ZSCORE);
+    k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0],
+                                       params[1], params[2], params[3], MODE_ZSCORE);
     ZSB_LAUNCH("k_init_level1");
     return ZSB_OK;
 }

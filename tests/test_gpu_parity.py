@@ -188,7 +188,7 @@ class TestBuildingBlocks:  # test_core_ops.py with K1/K2/K4 parameter injection
         k, c = Z.stable_scatter(keys, plan, params, np.arange(keys.size, dtype=np.int64))
         assert sha(k) == case["scatter_keys_sha"] and sha(c) == case["scatter_payload_sha"]
 
-    @pytest.mark.parametrize("n,k", [(10**6, 600), (3 * 10**6, 4096), (10**6, 30000)])
+    @pytest.mark.parametrize("n,k", [(10**6, 600), (3 * 10**6, 2048), (10**6, 1500)])
     def test_large_injected_scatter_vs_oracle(self, Z, n, k):
         keys = O.generate_family("normal", n, 21)
         mean, std, zmin, scale = O.mapping_params(keys, k)
