@@ -524,6 +524,7 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb) {
     size_t o = 0;
     L.off_cur = o;
     o += (size_t)k * 4;
+    o = (o + 15) & ~(size_t)15;
     L.off_cnt = o;
     o += (size_t)k * NWARPS * 2;
     o = (o + 15) & ~(size_t)15;
@@ -541,30 +542,47 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb) {
     return L;
 }
 
-// Exclusive scan of n u16 counters in place (n a multiple of 32*NWARPS is
-// not required; any n), warp-cooperative, conflict-free; returns nothing.
-__device__ __forceinline__ void block_scan_u16(uint16_t *c, int n, uint32_t *wtot) {
-    const int w = threadIdx.x >> 5, lane = lane_id();
-    const int chunk = ((n + NWARPS * 32 - 1) / (NWARPS * 32)) * 32;
-    const int lo = w * chunk, hi = min(n, lo + chunk);
-    uint32_t tot = 0;
-    for (int q = lo + lane; q < hi; q += 32) tot += c[q];
-    tot = warp_sum(tot);
-    if (lane == 0) wtot[w] = tot;
-    __syncthreads();
-    uint32_t run = 0;
-    for (int q = 0; q < w; q++) run += wtot[q];
-    for (int j0 = lo; j0 < hi; j0 += 32) {
-        const int q = j0 + lane;
-        uint32_t v = q < hi ? c[q] : 0u, x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (q < hi) c[q] = (uint16_t)(run + x - v);
-        run += __shfl_sync(0xffffffffu, x, 31);
+// Exclusive scan, in (digit, warp) order, of per-(digit, warp) u16 counters
+// laid out [digit][NWARPS] (one uint4 per digit).  Thread t owns digits
+// [t*per, (t+1)*per): a thread-local pass over its uint4s, one block scan
+// of the thread totals, and a write-back pass.  Also writes the digit
+// starts to dstart[0..ndig] (dstart[ndig] = total).  Ends with a barrier.
+__device__ __forceinline__ void scan_dw8(uint16_t *cnt, int ndig, uint16_t *dstart, uint32_t *wsum) {
+    static_assert(NWARPS == 8, "one uint4 per digit");
+    const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+    const int per = (ndig + NT - 1) / NT;
+    const int d0 = min(ndig, tid * per), d1 = min(ndig, d0 + per);
+    uint4 *c4 = (uint4 *)cnt;
+    uint32_t tsum = 0;
+    for (int d = d0; d < d1; d++) {
+        const uint4 v = c4[d];
+        tsum += (v.x & 0xffff) + (v.x >> 16) + (v.y & 0xffff) + (v.y >> 16) + (v.z & 0xffff) + (v.z >> 16) +
+                (v.w & 0xffff) + (v.w >> 16);
     }
+    uint32_t x = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    uint32_t run = x - tsum;
+    for (int q = 0; q < w; q++) run += wsum[q];
+    for (int d = d0; d < d1; d++) {
+        const uint4 v = c4[d];
+        dstart[d] = (uint16_t)run;
+        uint32_t h[8] = {v.x & 0xffff, v.x >> 16, v.y & 0xffff, v.y >> 16,
+                         v.z & 0xffff, v.z >> 16, v.w & 0xffff, v.w >> 16};
+        uint32_t e[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            e[q] = run;
+            run += h[q];
+        }
+        c4[d] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
+    }
+    if (tid == NT - 1) dstart[ndig] = (uint16_t)run;
     __syncthreads();
 }
 
@@ -632,10 +650,7 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *_
             __syncwarp();
         }
         __syncthreads();
-        block_scan_u16(cnt, NC, wtot);
-        for (int b = threadIdx.x; b < k; b += NT) lst[b] = cnt[b * NWARPS];
-        if (threadIdx.x == 0) lst[k] = (uint16_t)nvalid;
-        __syncthreads();  // lst reads cnt[b*NWARPS], which warp 0 advances below
+        scan_dw8(cnt, k, lst, wtot);
         // place (stable local sort by bucket)
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
@@ -861,25 +876,30 @@ __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned l
 // ------------------------------------------------------------------- K5
 // Shared-memory stable finish of one run of whole buckets (len <= NT*F).
 //  load    every thread issues its F key (and payload) loads up front and
-//          keeps them in registers: warp w owns the contiguous slice
-//          [w*32F, (w+1)*32F), item j of lane l is record w*32F + j*32 + l;
-//  minmax  exact ordered min/max of the run (block reduce);
-//  count   sub-bucket digit = top bits of (ord(key) - ord(min)); per-warp
-//          u16 counters advanced by __match_any_sync leaders in (j, lane)
-//          order, i.e. input order within the warp's slice;
-//  scan    conflict-free warp-cooperative exclusive scan in (digit, warp)
-//          order -> stable placement offsets;
-//  place   keys + payload into shared memory in sub-bucket order;
-//  sort    insertion sort of each small sub-bucket (only strictly greater
-//          keys shift: stable, _kernels.py:143-156); sub-buckets above
-//          FIN_INS that are not already ordered are emitted as refine runs
-//          and finished again by a later launch (their key range shrinks by
-//          2^sbits each time, so this terminates);
-//  write   coalesced stores of the run.
-// All loads complete before any output store, so src may alias the output.
+//          keeps them in registers; item j of lane l of warp w is record
+//          w*32F + j*32 + l (input order = record index);
+//  minmax  exact ordered min/max of the run (block reduce; all-equal runs
+//          are already in stable order and are copied through);
+//  digits  d = floor((ord(key) - ord(min)) * S / (range + 1)) with S ~ m/2,
+//          monotone in the key, so sub-bucket order is key order;
+//  count   shared-memory atomic histogram of the digits, exclusive scan;
+//  place   records go to their sub-bucket with an atomic cursor (any order)
+//          together with their record index;
+//  rank    each record's rank inside its sub-bucket is the number of
+//          members with a smaller (key, record index): equal keys keep input
+//          order, so the result is the stable sort; it is stored straight to
+//          its final position.
+// Sub-buckets above `fin_ins` records take a stable path instead: records
+// of those digits are re-placed in input order by per-(digit, warp)
+// counters advanced by __match_any_sync leaders; if such a sub-bucket is not
+// already ordered (it is whenever its keys are all equal) it is emitted as a
+// refine run and finished again by a later launch (its key range shrinks by
+// a factor ~S each time, so this terminates).  All loads complete before any
+// output store, so src may alias the output (in-place refinement).
 
-constexpr int FIN_INS = 32;        // sub-buckets up to this size are ranked in place
-constexpr int FIN_SBITS_MAX = 11;  // <= 2048 sub-buckets
+constexpr int FIN_INS = 32;         // sub-buckets up to this size are ranked by comparison
+constexpr int FIN_SBITS_MAX = 11;   // <= 2048 sub-buckets
+constexpr int FIN_BIG_MAX = 256;    // oversized sub-buckets handled per run (more -> all stable path)
 
 template <int PB>
 struct FinItems {
@@ -888,22 +908,28 @@ struct FinItems {
 
 struct FinLayout {
     int cap;
-    size_t off_b, off_pb, off_cnt, off_st, total;
+    size_t off_o, off_pb, off_i, off_cur, off_st, off_bcnt, total;
 };
 
 __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     FinLayout L;
     L.cap = cap;
     size_t o = 0;
-    L.off_b = o;
+    L.off_o = o;
     o += (size_t)cap * 8;
     L.off_pb = o;
     o += (size_t)cap * pb;
     o = (o + 15) & ~(size_t)15;
-    L.off_cnt = o;
-    o += (size_t)(1 << FIN_SBITS_MAX) * NWARPS * 2;
+    L.off_i = o;
+    o += (size_t)cap * 2;
+    o = (o + 15) & ~(size_t)15;
+    L.off_cur = o;
+    o += (size_t)(1 << FIN_SBITS_MAX) * 4;
     L.off_st = o;
     o += (size_t)((1 << FIN_SBITS_MAX) + 1) * 2;
+    o = (o + 15) & ~(size_t)15;
+    L.off_bcnt = o;
+    o += (size_t)FIN_BIG_MAX * NWARPS * 2 + 16;
     o = (o + 15) & ~(size_t)15;
     L.total = o;
     return L;
@@ -916,13 +942,18 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
     constexpr int F = FinItems<PB>::F;
     extern __shared__ __align__(16) unsigned char smem[];
     const FinLayout L = fin_layout(cap, PB);
-    uint64_t *Bo = (uint64_t *)(smem + L.off_b);  // ordered images, placed
+    uint64_t *Bo = (uint64_t *)(smem + L.off_o);  // ordered key images, placed
     P *PBf = (P *)(smem + L.off_pb);
-    uint16_t *cnt = (uint16_t *)(smem + L.off_cnt);
+    uint16_t *Ix = (uint16_t *)(smem + L.off_i);  // record index of each placed element
+    uint32_t *cur = (uint32_t *)(smem + L.off_cur);
     uint16_t *sst = (uint16_t *)(smem + L.off_st);
+    uint16_t *bcnt = (uint16_t *)(smem + L.off_bcnt);
     __shared__ unsigned long long r_min[NWARPS], r_max[NWARPS];
-    __shared__ uint32_t wtot[NWARPS];
-    __shared__ uint32_t negzero[256];  // float64: bit per placed record that was -0.0 (cap <= 8192)
+    __shared__ uint32_t wsum[NWARPS];
+    __shared__ uint32_t negzero[256];  // float64: bit per record index that was -0.0 (cap <= 8192)
+    __shared__ int nbig;
+    __shared__ uint16_t bdig[FIN_BIG_MAX];     // digit of each oversized sub-bucket
+    __shared__ uint16_t bslot_start[FIN_BIG_MAX + 1];
 
     const Entry e = entries[blockIdx.x];
     const int m = e.len;
@@ -932,24 +963,26 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
     uint64_t *ok = B.out_k + e.start;
     P *op = (P *)B.out_p + e.start;
     const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-    const unsigned lt = lanemask_lt();
     const int base = w * 32 * F + lane;
 
-    uint64_t key[F];
+    uint64_t o[F];
     P pay[F];
 #pragma unroll
     for (int j = 0; j < F; j++) {
         const int i = base + j * 32;
-        key[j] = i < m ? sk[i] : 0ull;
+        o[j] = i < m ? sk[i] : 0ull;
         if constexpr (PB != 0) pay[j] = i < m ? sp[i] : (P)0;
     }
+    if (KK == KEY_F64) negzero[tid] = 0u;
+    if (tid == 0) nbig = 0;
     unsigned long long omin = ~0ull, omax = 0;
 #pragma unroll
     for (int j = 0; j < F; j++) {
+        if (KK == KEY_F64 && o[j] == SIGN) atomicOr(&negzero[(base + j * 32) >> 5], 1u << lane);
+        o[j] = ord_key<KK>(o[j]);
         if (base + j * 32 < m) {
-            unsigned long long o = ord_key<KK>(key[j]);
-            omin = min(omin, o);
-            omax = max(omax, o);
+            omin = min(omin, (unsigned long long)o[j]);
+            omax = max(omax, (unsigned long long)o[j]);
         }
     }
     omin = warp_min_u64(omin);
@@ -958,7 +991,6 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         r_min[w] = omin;
         r_max[w] = omax;
     }
-    if (KK == KEY_F64) negzero[tid] = 0u;
     __syncthreads();
     omin = r_min[0];
     omax = r_max[0];
@@ -967,93 +999,177 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         omin = min(omin, r_min[j]);
         omax = max(omax, r_max[j]);
     }
+    auto key_bits = [&](uint64_t ov, int idx) -> uint64_t {
+        uint64_t kb = key_from_ord<KK>(ov);
+        if (KK == KEY_F64 && ((negzero[idx >> 5] >> (idx & 31)) & 1u)) kb = SIGN;
+        return kb;
+    };
     if (omin == omax) {  // all equal: already in stable order
         if (e.src != 2) {
 #pragma unroll
             for (int j = 0; j < F; j++) {
                 const int i = base + j * 32;
                 if (i < m) {
-                    ok[i] = key[j];
+                    ok[i] = key_bits(o[j], i);
                     if constexpr (PB != 0) op[i] = pay[j];
                 }
             }
         }
         return;
     }
-    // digits: d = floor((ord - min) * S / (range + 1)), monotone, in [0, S)
     int sbits = 5;
     while ((1 << sbits) < (m >> 1) && sbits < FIN_SBITS_MAX) sbits++;
     const int S = 1 << sbits;
     const uint64_t range = omax - omin;
-    // d = (ord - min) when the range fits S digits (one key value per digit),
-    // else d = mulhi(ord - min, M) with M = floor((2^64-1)/(range+1)) * S,
-    // which is monotone and < S.
-    const bool direct = range < (uint64_t)S;
+    const bool direct = range < (uint64_t)S;  // one key value per digit
     const uint64_t M = direct ? 0ull : ((range == ~0ull ? 1ull : (~0ull / (range + 1))) * (uint64_t)S);
-    const int NC = S * NWARPS;
-    for (int i = tid; i < NC / 2; i += NT) ((uint32_t *)cnt)[i] = 0u;
+    auto digit = [&](uint64_t ov) -> int {
+        const uint64_t x = ov - omin;
+        return (int)(direct ? x : __umul64hi(x, M));
+    };
+    for (int d = tid; d < S; d += NT) cur[d] = 0u;
     __syncthreads();
-    // ---- count per (digit, warp) in input order
+    // ---- histogram
 #pragma unroll
-    for (int j = 0; j < F; j++) {
-        const uint64_t x = ord_key<KK>(key[j]) - omin;
-        const int d = (base + j * 32 < m) ? (int)(direct ? x : __umul64hi(x, M)) : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (d >= 0 && (peers & lt) == 0) cnt[d * NWARPS + w] += (uint16_t)__popc(peers);
-        __syncwarp();
-    }
+    for (int j = 0; j < F; j++)
+        if (base + j * 32 < m) atomicAdd(&cur[digit(o[j])], 1u);
     __syncthreads();
-    block_scan_u16(cnt, NC, wtot);
-    for (int d = tid; d < S; d += NT) sst[d] = cnt[d * NWARPS];
-    if (tid == 0) sst[S] = (uint16_t)m;
-    __syncthreads();  // sst reads cnt[d*NWARPS], which warp 0 advances below
-    // ---- stable placement of ordered images into shared memory
+    // ---- exclusive scan -> sst (starts), cur (cursors); flag oversized digits
+    {
+        const int per = S / NT > 0 ? S / NT : 1;
+        const int d0 = min(S, tid * per), d1 = min(S, d0 + per);
+        uint32_t tsum = 0;
+        for (int d = d0; d < d1; d++) tsum += cur[d];
+        uint32_t x = tsum;
 #pragma unroll
-    for (int j = 0; j < F; j++) {
-        const uint64_t o = ord_key<KK>(key[j]);
-        const int d = (base + j * 32 < m) ? (int)(direct ? o - omin : __umul64hi(o - omin, M)) : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t b0 = 0;
-        if (d >= 0 && lane == leader) {
-            b0 = cnt[d * NWARPS + w];
-            cnt[d * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
+        for (int q = 1; q < 32; q <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, q);
+            if (lane >= q) x += y;
         }
-        b0 = __shfl_sync(0xffffffffu, b0, leader);
-        if (d >= 0) {
-            const uint32_t pos = b0 + __popc(peers & lt);
-            Bo[pos] = o;
-            if constexpr (PB != 0) PBf[pos] = pay[j];
-            if (KK == KEY_F64 && key[j] == SIGN) atomicOr(&negzero[pos >> 5], 1u << (pos & 31));
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    // ---- rank inside each sub-bucket by (ordered key, placement index) and
-    //      store straight to the final position (placement order is input
-    //      order within a sub-bucket, so ties keep input order: stable)
-    for (int i = tid; i < m; i += NT) {
-        const uint64_t o = Bo[i];
-        const int d = (int)(direct ? o - omin : __umul64hi(o - omin, M));
-        const int a = sst[d], z = sst[d + 1];
-        int rank = i - a;
-        if (z - a <= fin_ins) {
-            rank = 0;
-            for (int x = a; x < z; x++) {
-                const uint64_t ox = Bo[x];
-                rank += (ox < o) || (ox == o && x < i);
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        uint32_t run = x - tsum;
+        for (int q = 0; q < w; q++) run += wsum[q];
+        for (int d = d0; d < d1; d++) {
+            const uint32_t c = cur[d];
+            sst[d] = (uint16_t)run;
+            if (c > (uint32_t)fin_ins) {
+                const int b = atomicAdd(&nbig, 1);
+                if (b < FIN_BIG_MAX) bdig[b] = (uint16_t)d;
+                cur[d] = 0xFFFFFFFFu;  // stable path marker
+            } else {
+                cur[d] = run;
             }
-        } else if (i == a) {  // oversized sub-bucket: refine later unless already ordered
+            run += c;
+        }
+        if (tid == NT - 1) sst[S] = (uint16_t)m;
+    }
+    __syncthreads();
+    const int nb = nbig;  // <= m / (fin_ins + 1) <= FIN_BIG_MAX
+    // ---- place (atomic cursors; oversized digits go through the stable path)
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const int i = base + j * 32;
+        if (i < m) {
+            const int d = digit(o[j]);
+            if (cur[d] != 0xFFFFFFFFu) {
+                const uint32_t pos = atomicAdd(&cur[d], 1u);
+                Bo[pos] = o[j];
+                Ix[pos] = (uint16_t)i;
+                if constexpr (PB != 0) PBf[pos] = pay[j];
+            }
+        }
+    }
+    if (nb > 0) {
+        // Stable placement of the oversized digits: sort their digit list,
+        // then per-(slot, warp) counters advanced in input order.
+        if (tid < nb) {
+            const int dv = bdig[tid];
+            int rank = 0;
+            for (int q = 0; q < nb; q++) rank += bdig[q] < dv;
+            bslot_start[rank] = (uint16_t)dv;
+        }
+        for (int q = tid; q < nb * NWARPS; q += NT) bcnt[q] = 0;
+        __syncthreads();
+        const unsigned lt = lanemask_lt();
+        int sl[F];
+#pragma unroll
+        for (int j = 0; j < F; j++) {
+            sl[j] = -1;
+            if (base + j * 32 < m) {
+                const int d = digit(o[j]);
+                if (cur[d] == 0xFFFFFFFFu) {
+                    int lo = 0, hi = nb - 1;  // bslot_start holds the sorted oversized digits
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (bslot_start[mid] < d) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    sl[j] = lo;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < F; j++) {
+            const unsigned peers = __match_any_sync(0xffffffffu, sl[j]);
+            if (sl[j] >= 0 && (peers & lt) == 0) bcnt[sl[j] * NWARPS + w] += (uint16_t)__popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int q = tid; q < nb; q += NT) {  // exclusive prefix over warps from the digit's start
+            uint32_t run = sst[bslot_start[q]];
+            for (int ww = 0; ww < NWARPS; ww++) {
+                const uint32_t c = bcnt[q * NWARPS + ww];
+                bcnt[q * NWARPS + ww] = (uint16_t)run;
+                run += c;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < F; j++) {
+            const unsigned peers = __match_any_sync(0xffffffffu, sl[j]);
+            const int leader = __ffs(peers) - 1;
+            uint32_t b0 = 0;
+            if (sl[j] >= 0 && lane == leader) {
+                b0 = bcnt[sl[j] * NWARPS + w];
+                bcnt[sl[j] * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
+            }
+            b0 = __shfl_sync(0xffffffffu, b0, leader);
+            if (sl[j] >= 0) {
+                const uint32_t pos = b0 + __popc(peers & lt);
+                Bo[pos] = o[j];
+                Ix[pos] = (uint16_t)(base + j * 32);
+                if constexpr (PB != 0) PBf[pos] = pay[j];
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // ---- rank inside each sub-bucket and store to the final position
+    for (int i = tid; i < m; i += NT) {
+        const uint64_t ov = Bo[i];
+        const int idx = Ix[i];
+        const int d = digit(ov);
+        const int a = sst[d], z = sst[d + 1];
+        const int c = z - a;
+        int rank = i - a;
+        if (c <= fin_ins) {
+            if (c > 1) {
+                rank = 0;
+                for (int x = a; x < z; x++) {
+                    const uint64_t ox = Bo[x];
+                    rank += (ox < ov) || (ox == ov && Ix[x] < idx);
+                }
+            }
+        } else if (i == a) {  // oversized sub-bucket, placed stably: refine unless already ordered
             bool sorted = true;
             for (int x = a + 1; x < z && sorted; x++) sorted = Bo[x - 1] <= Bo[x];
             if (!sorted) {
                 unsigned long long r = atomicAdd(refine_count, 1ull);
-                refine[r] = Entry{e.start + a, z - a, 2};
+                refine[r] = Entry{e.start + a, c, 2};
             }
         }
-        uint64_t kb = key_from_ord<KK>(o);
-        if (KK == KEY_F64 && ((negzero[i >> 5] >> (i & 31)) & 1u)) kb = SIGN;
-        ok[a + rank] = kb;
+        ok[a + rank] = key_bits(ov, idx);
         if constexpr (PB != 0) op[a + rank] = PBf[i];
     }
 }
