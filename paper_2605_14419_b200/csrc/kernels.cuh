@@ -642,33 +642,37 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *_
         }
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p) : -1;
-        // count per (bucket, warp) in input order
+        // count per (bucket, warp): all MATCH.ANY issued back to back, the
+        // leaders add with shared atomics on the containing 32-bit word
+        unsigned peers[ITEMS];
+#pragma unroll
+        for (int j = 0; j < ITEMS; j++) peers[j] = __match_any_sync(0xffffffffu, bk[j]);
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const unsigned peers = __match_any_sync(0xffffffffu, bk[j]);
-            if (bk[j] >= 0 && (peers & lt) == 0) cnt[bk[j] * NWARPS + w] += (uint16_t)__popc(peers);
-            __syncwarp();
+            if (bk[j] >= 0 && (peers[j] & lt) == 0) {
+                const int q = bk[j] * NWARPS + w;
+                atomicAdd((uint32_t *)cnt + (q >> 1), (uint32_t)__popc(peers[j]) << (16 * (q & 1)));
+            }
         }
         __syncthreads();
         scan_dw8(cnt, k, lst, wtot);
-        // place (stable local sort by bucket)
+        // place (stable local sort by bucket): items in input order
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const unsigned peers = __match_any_sync(0xffffffffu, bk[j]);
-            const int leader = __ffs(peers) - 1;
+            const int leader = __ffs(peers[j]) - 1;
             uint32_t b0 = 0;
             if (bk[j] >= 0 && lane == leader) {
                 b0 = cnt[bk[j] * NWARPS + w];
-                cnt[bk[j] * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
+                cnt[bk[j] * NWARPS + w] = (uint16_t)(b0 + __popc(peers[j]));
             }
+            __syncwarp();
             b0 = __shfl_sync(0xffffffffu, b0, leader);
             if (bk[j] >= 0) {
-                const uint32_t pos = b0 + __popc(peers & lt);
+                const uint32_t pos = b0 + __popc(peers[j] & lt);
                 stk[pos] = key[j];
                 if constexpr (PB != 0) stp[pos] = pay[j];
                 stb[pos] = (uint16_t)bk[j];
             }
-            __syncwarp();
         }
         __syncthreads();
         // coalesced run writes, counters reset for the next round
@@ -898,12 +902,15 @@ __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned l
 // output store, so src may alias the output (in-place refinement).
 
 constexpr int FIN_INS = 32;         // sub-buckets up to this size are ranked by comparison
-constexpr int FIN_SBITS_MAX = 11;   // <= 2048 sub-buckets
-constexpr int FIN_BIG_MAX = 256;    // oversized sub-buckets handled per run (more -> all stable path)
+constexpr int FIN_SBITS_MAX = 12;   // <= 4096 sub-buckets (16-bit cursors)
+constexpr int FIN_BIG_MAX = 256;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
+
+constexpr int FT = 512;         // threads per finish CTA
+constexpr int FW = FT / 32;     // warps per finish CTA
 
 template <int PB>
 struct FinItems {
-    static constexpr int F = PB == 8 ? 16 : (PB == 4 ? 24 : 32);
+    static constexpr int F = PB == 8 ? 8 : (PB == 4 ? 12 : 16);  // records per thread; cap = FT * F
 };
 
 struct FinLayout {
@@ -923,21 +930,27 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     L.off_i = o;
     o += (size_t)cap * 2;
     o = (o + 15) & ~(size_t)15;
-    L.off_cur = o;
-    o += (size_t)(1 << FIN_SBITS_MAX) * 4;
+    L.off_cur = o;  // S 16-bit counters/cursors, packed two per word
+    o += (size_t)(1 << FIN_SBITS_MAX) * 2;
     L.off_st = o;
-    o += (size_t)((1 << FIN_SBITS_MAX) + 1) * 2;
+    o += (size_t)((1 << FIN_SBITS_MAX) + 2) * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_bcnt = o;
-    o += (size_t)FIN_BIG_MAX * NWARPS * 2 + 16;
+    o += (size_t)FIN_BIG_MAX * FW * 2 + (1 << FIN_SBITS_MAX) / 8 + 16;
     o = (o + 15) & ~(size_t)15;
     L.total = o;
     return L;
 }
 
 template <int KK, int PB>
-__global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__restrict__ entries, int cap,
-                                                  Entry *refine, unsigned long long *refine_count, int fin_ins) {
+__global__ void __launch_bounds__(FT, 2) k_finish(Buffers B, const Entry *__restrict__ entries, int cap,
+                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
+                                                  long long *prof) {
+#define FIN_MARK(slot)                                                                                   \
+    do {                                                                                                 \
+        if (prof && threadIdx.x == 0) prof[(int64_t)blockIdx.x * 8 + (slot)] = clock64();              \
+    } while (0)
+    FIN_MARK(0);
     using P = typename PayloadT<PB>::T;
     constexpr int F = FinItems<PB>::F;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -945,15 +958,15 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
     uint64_t *Bo = (uint64_t *)(smem + L.off_o);  // ordered key images, placed
     P *PBf = (P *)(smem + L.off_pb);
     uint16_t *Ix = (uint16_t *)(smem + L.off_i);  // record index of each placed element
-    uint32_t *cur = (uint32_t *)(smem + L.off_cur);
+    uint32_t *cw = (uint32_t *)(smem + L.off_cur);  // 16-bit counters, two per word
     uint16_t *sst = (uint16_t *)(smem + L.off_st);
     uint16_t *bcnt = (uint16_t *)(smem + L.off_bcnt);
-    __shared__ unsigned long long r_min[NWARPS], r_max[NWARPS];
-    __shared__ uint32_t wsum[NWARPS];
+    uint32_t *bigmask = (uint32_t *)(smem + L.off_bcnt + FIN_BIG_MAX * FW * 2);
+    __shared__ unsigned long long r_min[FW], r_max[FW];
+    __shared__ uint32_t wsum[FW];
     __shared__ uint32_t negzero[256];  // float64: bit per record index that was -0.0 (cap <= 8192)
     __shared__ int nbig;
-    __shared__ uint16_t bdig[FIN_BIG_MAX];     // digit of each oversized sub-bucket
-    __shared__ uint16_t bslot_start[FIN_BIG_MAX + 1];
+    __shared__ uint16_t bslot[FIN_BIG_MAX];  // sorted oversized digits
 
     const Entry e = entries[blockIdx.x];
     const int m = e.len;
@@ -973,12 +986,16 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         o[j] = i < m ? sk[i] : 0ull;
         if constexpr (PB != 0) pay[j] = i < m ? sp[i] : (P)0;
     }
-    if (KK == KEY_F64) negzero[tid] = 0u;
     if (tid == 0) nbig = 0;
+    bool anyneg = false;
+    if constexpr (KK == KEY_F64) {
+        if (tid < 256) negzero[tid] = 0u;
+#pragma unroll
+        for (int j = 0; j < F; j++) anyneg |= (o[j] == SIGN);
+    }
     unsigned long long omin = ~0ull, omax = 0;
 #pragma unroll
     for (int j = 0; j < F; j++) {
-        if (KK == KEY_F64 && o[j] == SIGN) atomicOr(&negzero[(base + j * 32) >> 5], 1u << lane);
         o[j] = ord_key<KK>(o[j]);
         if (base + j * 32 < m) {
             omin = min(omin, (unsigned long long)o[j]);
@@ -991,17 +1008,27 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         r_min[w] = omin;
         r_max[w] = omax;
     }
-    __syncthreads();
+    if constexpr (KK == KEY_F64) anyneg = __syncthreads_or(anyneg);
+    else __syncthreads();
+    if constexpr (KK == KEY_F64) {
+        if (anyneg) {  // -0.0 and +0.0 share an ordered image; remember which records were -0.0
+#pragma unroll
+            for (int j = 0; j < F; j++)
+                if (base + j * 32 < m && o[j] == ord_key<KK>(SIGN) && sk[base + j * 32] == SIGN)
+                    atomicOr(&negzero[(base + j * 32) >> 5], 1u << lane);
+            __syncthreads();
+        }
+    }
     omin = r_min[0];
     omax = r_max[0];
 #pragma unroll
-    for (int j = 1; j < NWARPS; j++) {
+    for (int j = 1; j < FW; j++) {
         omin = min(omin, r_min[j]);
         omax = max(omax, r_max[j]);
     }
     auto key_bits = [&](uint64_t ov, int idx) -> uint64_t {
         uint64_t kb = key_from_ord<KK>(ov);
-        if (KK == KEY_F64 && ((negzero[idx >> 5] >> (idx & 31)) & 1u)) kb = SIGN;
+        if (KK == KEY_F64 && anyneg && ((negzero[idx >> 5] >> (idx & 31)) & 1u)) kb = SIGN;
         return kb;
     };
     if (omin == omax) {  // all equal: already in stable order
@@ -1018,28 +1045,64 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         return;
     }
     int sbits = 5;
-    while ((1 << sbits) < (m >> 1) && sbits < FIN_SBITS_MAX) sbits++;
+    while ((1 << sbits) < m && sbits < FIN_SBITS_MAX) sbits++;
     const int S = 1 << sbits;
     const uint64_t range = omax - omin;
     const bool direct = range < (uint64_t)S;  // one key value per digit
-    const uint64_t M = direct ? 0ull : ((range == ~0ull ? 1ull : (~0ull / (range + 1))) * (uint64_t)S);
+    // d = ((ord - min) >> sh) * M >> 32 with the shifted range below 2^32:
+    // monotone in the key and < S; 32-bit multiply only
+    const int sh = max(0, bitlen64(range) - 32);
+    const uint32_t r32 = (uint32_t)(range >> sh);
+    const uint32_t M = direct ? 0u : (uint32_t)((((uint64_t)S) << 32) / ((uint64_t)r32 + 1));
     auto digit = [&](uint64_t ov) -> int {
         const uint64_t x = ov - omin;
-        return (int)(direct ? x : __umul64hi(x, M));
+        return direct ? (int)x : (int)__umulhi((uint32_t)(x >> sh), M);
     };
-    for (int d = tid; d < S; d += NT) cur[d] = 0u;
+    for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
+    for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
     __syncthreads();
-    // ---- histogram
+    FIN_MARK(1);
+    // ---- histogram (16-bit counters: no carry, counts <= cap < 2^16)
+    uint32_t dpk[(F + 1) / 2];  // digits, two per register
 #pragma unroll
-    for (int j = 0; j < F; j++)
-        if (base + j * 32 < m) atomicAdd(&cur[digit(o[j])], 1u);
+    for (int j = 0; j < F; j++) {
+        const int d = (base + j * 32 < m) ? digit(o[j]) : 0xFFFF;
+        if (j & 1) dpk[j >> 1] |= (uint32_t)d << 16;
+        else dpk[j >> 1] = (uint32_t)d;
+        if (d != 0xFFFF) atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
+    }
     __syncthreads();
-    // ---- exclusive scan -> sst (starts), cur (cursors); flag oversized digits
+    FIN_MARK(2);
+    // ---- exclusive scan -> sst (starts) and cursors; flag oversized digits.
+    //      Thread t owns digits [t*per, (t+1)*per) (per = S/FT, 0 or a
+    //      multiple of 8 except when S < FT*8); 16-byte vector accesses.
     {
-        const int per = S / NT > 0 ? S / NT : 1;
-        const int d0 = min(S, tid * per), d1 = min(S, d0 + per);
+        uint16_t *c16 = (uint16_t *)cw;
+        const int per = S / FT;  // S >= 32; per in {0 (S<FT), 1, 2, 4, 8}
+        const int d0 = per ? tid * per : (tid < S ? tid : S), d1 = per ? d0 + per : (tid < S ? tid + 1 : S);
+        uint16_t v[16];
         uint32_t tsum = 0;
-        for (int d = d0; d < d1; d++) tsum += cur[d];
+        if (per >= 8) {
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                if (q * 8 < per) {
+                    const uint4 u = *(const uint4 *)(c16 + d0 + q * 8);
+                    const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        v[q * 8 + 2 * r] = (uint16_t)(wv[r] & 0xffff);
+                        v[q * 8 + 2 * r + 1] = (uint16_t)(wv[r] >> 16);
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+                if (q < d1 - d0) v[q] = c16[d0 + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q++)
+            if (q < d1 - d0) tsum += v[q];
         uint32_t x = tsum;
 #pragma unroll
         for (int q = 1; q < 32; q <<= 1) {
@@ -1050,103 +1113,128 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         __syncthreads();
         uint32_t run = x - tsum;
         for (int q = 0; q < w; q++) run += wsum[q];
-        for (int d = d0; d < d1; d++) {
-            const uint32_t c = cur[d];
-            sst[d] = (uint16_t)run;
-            if (c > (uint32_t)fin_ins) {
-                const int b = atomicAdd(&nbig, 1);
-                if (b < FIN_BIG_MAX) bdig[b] = (uint16_t)d;
-                cur[d] = 0xFFFFFFFFu;  // stable path marker
-            } else {
-                cur[d] = run;
+        uint16_t e[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+            if (q < d1 - d0) {
+                e[q] = (uint16_t)run;
+                if (v[q] > (uint32_t)fin_ins) {
+                    const int d = d0 + q;
+                    const int bi = atomicAdd(&nbig, 1);
+                    if (bi < FIN_BIG_MAX) bslot[bi] = (uint16_t)d;
+                    atomicOr(&bigmask[d >> 5], 1u << (d & 31));
+                }
+                run += v[q];
             }
-            run += c;
         }
-        if (tid == NT - 1) sst[S] = (uint16_t)m;
+        if (per >= 8) {
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                if (q * 8 < per) {
+                    const uint4 u = make_uint4(e[q * 8] | ((uint32_t)e[q * 8 + 1] << 16),
+                                               e[q * 8 + 2] | ((uint32_t)e[q * 8 + 3] << 16),
+                                               e[q * 8 + 4] | ((uint32_t)e[q * 8 + 5] << 16),
+                                               e[q * 8 + 6] | ((uint32_t)e[q * 8 + 7] << 16));
+                    *(uint4 *)(c16 + d0 + q * 8) = u;
+                    *(uint4 *)(sst + d0 + q * 8) = u;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+                if (q < d1 - d0) {
+                    c16[d0 + q] = e[q];
+                    sst[d0 + q] = e[q];
+                }
+        }
+        if (tid == FT - 1) sst[S] = (uint16_t)m;
     }
     __syncthreads();
     const int nb = nbig;  // <= m / (fin_ins + 1) <= FIN_BIG_MAX
+    FIN_MARK(3);
     // ---- place (atomic cursors; oversized digits go through the stable path)
 #pragma unroll
     for (int j = 0; j < F; j++) {
-        const int i = base + j * 32;
-        if (i < m) {
-            const int d = digit(o[j]);
-            if (cur[d] != 0xFFFFFFFFu) {
-                const uint32_t pos = atomicAdd(&cur[d], 1u);
-                Bo[pos] = o[j];
-                Ix[pos] = (uint16_t)i;
-                if constexpr (PB != 0) PBf[pos] = pay[j];
-            }
+        const int d = (int)((dpk[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
+        if (d != 0xFFFF && (nb == 0 || !((bigmask[d >> 5] >> (d & 31)) & 1u))) {
+            const uint32_t old = atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
+            const uint32_t pos = (old >> (16 * (d & 1))) & 0xFFFFu;
+            Bo[pos] = o[j];
+            Ix[pos] = (uint16_t)(base + j * 32);
+            if constexpr (PB != 0) PBf[pos] = pay[j];
         }
     }
     if (nb > 0) {
         // Stable placement of the oversized digits: sort their digit list,
         // then per-(slot, warp) counters advanced in input order.
+        __syncthreads();
         if (tid < nb) {
-            const int dv = bdig[tid];
+            const int dv = bslot[tid];
             int rank = 0;
-            for (int q = 0; q < nb; q++) rank += bdig[q] < dv;
-            bslot_start[rank] = (uint16_t)dv;
+            for (int q = 0; q < nb; q++) rank += bslot[q] < dv;
+            ((uint16_t *)bcnt)[FIN_BIG_MAX * FW - 1 - rank] = (uint16_t)dv;
         }
-        for (int q = tid; q < nb * NWARPS; q += NT) bcnt[q] = 0;
+        __syncthreads();
+        if (tid < nb) bslot[tid] = ((uint16_t *)bcnt)[FIN_BIG_MAX * FW - 1 - tid];
+        __syncthreads();
+        for (int q = tid; q < nb * FW; q += FT) bcnt[q] = 0;
         __syncthreads();
         const unsigned lt = lanemask_lt();
-        int sl[F];
+        auto slot_of = [&](int j) -> int {  // slot of item j's digit, -1 unless oversized
+            const int d = (int)((dpk[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
+            if (d == 0xFFFF || !((bigmask[d >> 5] >> (d & 31)) & 1u)) return -1;
+            int lo = 0, hi = nb - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (bslot[mid] < d) lo = mid + 1;
+                else hi = mid;
+            }
+            return lo;
+        };
 #pragma unroll
         for (int j = 0; j < F; j++) {
-            sl[j] = -1;
-            if (base + j * 32 < m) {
-                const int d = digit(o[j]);
-                if (cur[d] == 0xFFFFFFFFu) {
-                    int lo = 0, hi = nb - 1;  // bslot_start holds the sorted oversized digits
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (bslot_start[mid] < d) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    sl[j] = lo;
-                }
+            const int sl = slot_of(j);
+            const unsigned peers = __match_any_sync(0xffffffffu, sl);
+            if (sl >= 0 && (peers & lt) == 0) {
+                const int q = sl * FW + w;
+                atomicAdd((uint32_t *)bcnt + (q >> 1), (uint32_t)__popc(peers) << (16 * (q & 1)));
             }
         }
-#pragma unroll
-        for (int j = 0; j < F; j++) {
-            const unsigned peers = __match_any_sync(0xffffffffu, sl[j]);
-            if (sl[j] >= 0 && (peers & lt) == 0) bcnt[sl[j] * NWARPS + w] += (uint16_t)__popc(peers);
-            __syncwarp();
-        }
         __syncthreads();
-        for (int q = tid; q < nb; q += NT) {  // exclusive prefix over warps from the digit's start
-            uint32_t run = sst[bslot_start[q]];
-            for (int ww = 0; ww < NWARPS; ww++) {
-                const uint32_t c = bcnt[q * NWARPS + ww];
-                bcnt[q * NWARPS + ww] = (uint16_t)run;
+        for (int q = tid; q < nb; q += FT) {  // exclusive prefix over warps from the digit's start
+            uint32_t run = sst[bslot[q]];
+            for (int ww = 0; ww < FW; ww++) {
+                const uint32_t c = bcnt[q * FW + ww];
+                bcnt[q * FW + ww] = (uint16_t)run;
                 run += c;
             }
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < F; j++) {
-            const unsigned peers = __match_any_sync(0xffffffffu, sl[j]);
+            const int sl = slot_of(j);
+            const unsigned peers = __match_any_sync(0xffffffffu, sl);
             const int leader = __ffs(peers) - 1;
             uint32_t b0 = 0;
-            if (sl[j] >= 0 && lane == leader) {
-                b0 = bcnt[sl[j] * NWARPS + w];
-                bcnt[sl[j] * NWARPS + w] = (uint16_t)(b0 + __popc(peers));
+            if (sl >= 0 && lane == leader) {
+                b0 = bcnt[sl * FW + w];
+                bcnt[sl * FW + w] = (uint16_t)(b0 + __popc(peers));
             }
+            __syncwarp();
             b0 = __shfl_sync(0xffffffffu, b0, leader);
-            if (sl[j] >= 0) {
+            if (sl >= 0) {
                 const uint32_t pos = b0 + __popc(peers & lt);
                 Bo[pos] = o[j];
                 Ix[pos] = (uint16_t)(base + j * 32);
                 if constexpr (PB != 0) PBf[pos] = pay[j];
             }
-            __syncwarp();
         }
     }
     __syncthreads();
-    // ---- rank inside each sub-bucket and store to the final position
-    for (int i = tid; i < m; i += NT) {
+    FIN_MARK(4);
+    // ---- rank inside each sub-bucket by (key, record index) and store to
+    //      the final position; ties keep input order (stable)
+    for (int i = tid; i < m; i += FT) {
         const uint64_t ov = Bo[i];
         const int idx = Ix[i];
         const int d = digit(ov);
@@ -1172,6 +1260,9 @@ __global__ void __launch_bounds__(NT, 2) k_finish(Buffers B, const Entry *__rest
         ok[a + rank] = key_bits(ov, idx);
         if constexpr (PB != 0) op[a + rank] = PBf[i];
     }
+    FIN_MARK(5);
+    FIN_MARK(6);
+#undef FIN_MARK
 }
 
 // Entry builder for the small-n path (one finish over the whole input).

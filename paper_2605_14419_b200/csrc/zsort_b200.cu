@@ -115,7 +115,7 @@ constexpr int K_LEVEL1_MAX = KSCAT_MAX;  // fan-out of one scatter pass
 constexpr int KMAX_CHILD = 1024;
 constexpr int MIN_TILE = 8192;
 
-int finish_cap(int pb) { return NT * (pb == 8 ? FinItems<8>::F : (pb == 4 ? FinItems<4>::F : FinItems<0>::F)); }
+int finish_cap(int pb) { return FT * (pb == 8 ? FinItems<8>::F : (pb == 4 ? FinItems<4>::F : FinItems<0>::F)); }
 
 int64_t cluster_count(int64_t n, double alpha) {  // core.py:146-148
     double v = std::nearbyint(alpha * std::sqrt((double)n));
@@ -289,6 +289,39 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     return ZSB_OK;
 }
 
+// ZSB_FIN_PROFILE=1: per-CTA phase timestamps of the largest finish launch
+// are dumped to stderr (instrumentation only).
+long long *g_fin_prof = nullptr;
+int64_t g_fin_prof_n = 0;
+long long *fin_prof(int64_t n) {
+    if (!env_int("ZSB_FIN_PROFILE", 0) || n < g_fin_prof_n) return nullptr;
+    if (g_fin_prof) cudaFree(g_fin_prof);
+    cudaMalloc(&g_fin_prof, (size_t)n * 8 * 8);
+    cudaMemset(g_fin_prof, 0, (size_t)n * 8 * 8);
+    g_fin_prof_n = n;
+    return g_fin_prof;
+}
+
+void fin_prof_dump() {
+    if (!g_fin_prof) return;
+    std::vector<long long> h((size_t)g_fin_prof_n * 8);
+    cudaMemcpy(h.data(), g_fin_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    double acc[7] = {0};
+    int64_t cnt = 0;
+    for (int64_t b = 0; b < g_fin_prof_n; b++) {
+        const long long *t = &h[(size_t)b * 8];
+        if (!t[6]) continue;  // all-equal or empty runs exit early
+        cnt++;
+        for (int q = 1; q <= 6; q++) acc[q] += (double)(t[q] - t[q - 1]);
+    }
+    fprintf(stderr, "[zsb] finish phases over %lld CTAs (cycles): load+minmax %.0f hist %.0f scan %.0f place %.0f "
+                    "order %.0f store %.0f\n", (long long)cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+            acc[5] / cnt, acc[6] / cnt);
+    cudaFree(g_fin_prof);
+    g_fin_prof = nullptr;
+    g_fin_prof_n = 0;
+}
+
 template <int KK, int PB>
 int launch_finish(Ctx &c, const Entry *list, int64_t nentries, int ref_out) {
     if (nentries <= 0) return ZSB_OK;
@@ -298,9 +331,9 @@ int launch_finish(Ctx &c, const Entry *list, int64_t nentries, int ref_out) {
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     {
         PhaseScope ph(PH_FINISH, c.st);
-        k_finish<KK, PB><<<(unsigned)nentries, NT, FL.total, c.st>>>(c.B, list, (int)c.P.cap, refine,
+        k_finish<KK, PB><<<(unsigned)nentries, FT, FL.total, c.st>>>(c.B, list, (int)c.P.cap, refine,
                                                                      ctrl + (ref_out ? C_NREF1 : C_NREF0),
-                                                                     env_int("ZSB_FIN_INS", FIN_INS));
+                                                                     env_int("ZSB_FIN_INS", FIN_INS), fin_prof(nentries));
     }
     ZSB_LAUNCH("k_finish");
     return ZSB_OK;
@@ -448,6 +481,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     timing_collect();
     int rc3 = drain_refine((int64_t)h_ctrl[r ? C_NREF1 : C_NREF0]);
     if (rc3) return rc3;
+    if (env_int("ZSB_FIN_PROFILE", 0)) fin_prof_dump();
     stats[ZSB_STAT_MAX_DEPTH] = (int64_t)h_ctrl[C_ST_MAXDEPTH];
     stats[ZSB_STAT_FALLBACKS] = (int64_t)h_ctrl[C_ST_FALLBACKS];
     stats[ZSB_STAT_SCATTERS] = (int64_t)h_ctrl[C_ST_SCATTERS];

@@ -1,0 +1,17 @@
+# Produces the evidence committed under profiles/: bench line, per-kernel launch
+# list (device time + DRAM bytes), one `ncu --set full` capture of the hot kernels.
+set -u
+TAG=${1:-r01}
+mkdir -p gpurun_out
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,clocks.max.mem --format=csv > gpurun_out/${TAG}_gpu.txt
+timeout -s KILL 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+echo "bench rc=$?"
+$CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv \
+    --log-file gpurun_out/${TAG}_launches.csv $CMD > /dev/null 2>&1
+echo "launch list rc=$?"
+$CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_finish|k_hist|k_moments" -s 8 -c 6 \
+    -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
+echo "full rc=$?"
