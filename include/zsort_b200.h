@@ -122,6 +122,41 @@ int zsb_check_sorted(const void *d_in_keys, const void *d_out_keys, const void *
                      int32_t key_dtype, int64_t n, int64_t index_base, void *d_workspace, int64_t *h_result,
                      void *stream);
 
+/* ---- multi-GPU phases (one process per GPU; the NCCL collectives D1-D3 run
+ * between these calls from paper_2605_14419_b200/dist.py over
+ * torch.distributed).  All are stream-ordered on `stream`. ---- */
+
+/* D1 payload: d_out3 = {count, sum(x - shift), sum((x - shift)^2)} (double)
+ * and d_out_bits2 = ordered (order-preserving uint64) min and max of the
+ * local shard; both are initialised by the call.  Replaces first_pass +
+ * variance_pass (_kernels.py:28-71) for a shard. */
+int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double shift, double *d_out3,
+                      uint64_t *d_out_bits2, void *stream);
+
+/* D2 payload: histogram of the k global z-score buckets (params = {center,
+ * std, zmin, scale}, Eq. 1, _kernels.py:91-112) into d_counts (int64[k],
+ * zeroed by the call), k <= 16384. */
+int zsb_bucket_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k,
+                         int64_t *d_counts, void *stream);
+
+/* Ordered min/max of the local keys falling in each of nb (<= 32)
+ * candidate buckets (all-equal test before a cut inside a bucket). */
+int zsb_bucket_minmax(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k, int32_t nb,
+                      const int32_t *d_buckets, uint64_t *d_omin, uint64_t *d_omax, void *stream);
+
+/* D3 input: stable partition of the local shard into ncuts+1 destination
+ * ranks.  Record i (global index gidx_base + i) goes to the number of cuts
+ * c_j with (bucket(x), ord(x), gidx) >= (h_cut_bucket[j], h_cut_ord[j],
+ * h_cut_gidx[j]) lexicographically -- the global stable order -- so every
+ * destination receives its records in input order.  h_part_counts receives
+ * the ncuts+1 per-destination counts; blocks until done. */
+size_t zsb_partition_workspace_bytes(int64_t n, int32_t payload_bytes, int32_t nparts);
+int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes,
+                           int64_t n, const double *params, int64_t k, int64_t gidx_base, int32_t ncuts,
+                           const int32_t *h_cut_bucket, const uint64_t *h_cut_ord, const int64_t *h_cut_gidx,
+                           void *d_out_keys, void *d_out_payload, int64_t *h_part_counts, void *d_workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* Optional per-phase device timing of zsb_sort on the calling thread (CUDA
  * events around each launch group, on the sort's own stream).  Phase slots:
  * 0 moments, 1 histogram, 2 scan, 3 scatter, 4 classify+plan, 5 finish,

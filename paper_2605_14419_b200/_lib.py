@@ -37,6 +37,8 @@ EXPORTS = (
     "zsb_workspace_bytes", "zsb_sort", "zsb_moments", "zsb_histogram", "zsb_scatter",
     "zsb_check_workspace_bytes", "zsb_check_sorted", "zsb_last_error", "zsb_version",
     "zsb_timing_enable", "zsb_timing_read",
+    "zsb_local_moments", "zsb_bucket_histogram", "zsb_bucket_minmax", "zsb_partition_workspace_bytes",
+    "zsb_partition_to_ranks",
 )
 
 PHASES = ("moments", "histogram", "scan", "scatter", "classify", "finish", "recursion_stats", "misc")
@@ -71,6 +73,17 @@ def load(auto_build: bool = True):
     L.zsb_check_workspace_bytes.restype = SZ
     L.zsb_check_sorted.argtypes = [P, P, P, I32, I32, I64, I64, P, P, P]
     L.zsb_check_sorted.restype = ctypes.c_int
+    D = ctypes.c_double
+    L.zsb_local_moments.argtypes = [P, I32, I64, D, P, P, P]
+    L.zsb_local_moments.restype = ctypes.c_int
+    L.zsb_bucket_histogram.argtypes = [P, I32, I64, P, I64, P, P]
+    L.zsb_bucket_histogram.restype = ctypes.c_int
+    L.zsb_bucket_minmax.argtypes = [P, I32, I64, P, I64, I32, P, P, P, P]
+    L.zsb_bucket_minmax.restype = ctypes.c_int
+    L.zsb_partition_workspace_bytes.argtypes = [I64, I32, I32]
+    L.zsb_partition_workspace_bytes.restype = SZ
+    L.zsb_partition_to_ranks.argtypes = [P, I32, P, I32, I64, P, I64, I64, I32, P, P, P, P, P, P, P, SZ, P]
+    L.zsb_partition_to_ranks.restype = ctypes.c_int
     L.zsb_timing_enable.argtypes = [I32]
     L.zsb_timing_enable.restype = None
     L.zsb_timing_read.argtypes = [P, P, I32, I32]

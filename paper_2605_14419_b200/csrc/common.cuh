@@ -21,6 +21,24 @@ enum SegMode : int32_t {
     MODE_ZSCORE = 0,   // Eq. 1 z-score bucket (fp64, IEEE-exact intrinsics)
     MODE_INTEGER = 1,  // exact MSD digit of (ord(key) - ord(min)): termination fallback (K7)
     MODE_COPY = 2,     // all keys equal: copy through (core.py:377-380, _kernels.py:339-343)
+    MODE_DEST = 3,     // multi-GPU exchange: bucket = destination rank from the global cuts
+};
+
+// Global cuts of the multi-GPU exchange (paper_2605_14419_b200/dist.py).
+// A record (key x, global index g) goes to the number of cuts c_j with
+// (bucket(x), ord(x), g) >= (bucket_j, ord_j, gidx_j) lexicographically;
+// bucket(x) is the global fitted z-score bucket, monotone in x, so this
+// order is the global stable order (key, original index).
+constexpr int MAX_CUTS = 15;
+struct DestCuts {
+    double center, std, zmin, scale;
+    int32_t k;
+    int32_t ncuts;
+    int64_t gidx_base;
+    int32_t bucket[MAX_CUTS];
+    int32_t pad;
+    uint64_t ord[MAX_CUTS];
+    int64_t gidx[MAX_CUTS];
 };
 
 // Per-segment partition parameters (one partition problem of the batch).
@@ -125,9 +143,25 @@ __device__ __forceinline__ int32_t bucket_z(double x, double center, double std,
 }
 
 template <int KK>
-__device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p) {
+__device__ __forceinline__ int32_t dest_of(uint64_t bits, int64_t pos, const DestCuts *c) {
+    const int32_t b = bucket_z(key_value<KK>(bits), c->center, c->std, c->zmin, c->scale, c->k);
+    const uint64_t o = ord_key<KK>(bits);
+    const int64_t g = c->gidx_base + pos;
+    int32_t d = 0;
+    for (int j = 0; j < c->ncuts; j++) {
+        const bool ge = b > c->bucket[j] ||
+                        (b == c->bucket[j] && (o > c->ord[j] || (o == c->ord[j] && g >= c->gidx[j])));
+        d += ge;
+    }
+    return d;
+}
+
+template <int KK>
+__device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p, int64_t pos = 0,
+                                              const DestCuts *cuts = nullptr) {
     if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
     if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
+    if (p.mode == MODE_DEST) return dest_of<KK>(bits, pos, cuts);
     return 0;
 }
 

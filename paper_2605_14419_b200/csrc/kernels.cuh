@@ -29,6 +29,7 @@ struct Buffers {
     void *tmp_p;
     uint64_t *out_k;
     void *out_p;
+    const DestCuts *cuts;  // MODE_DEST only
 };
 
 __device__ __forceinline__ const uint64_t *src_keys(const Buffers &B, int src) {
@@ -402,9 +403,9 @@ __global__ void __launch_bounds__(NT) k_hist(Buffers B, const SegParams *__restr
 #pragma unroll
         for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * NT);
 #pragma unroll
-        for (int u = 0; u < 8; u++) atomicAdd(&hist[seg_bucket<KK>(b[u], p)], 1u);
+        for (int u = 0; u < 8; u++) atomicAdd(&hist[seg_bucket<KK>(b[u], p, i + u * NT, B.cuts)], 1u);
     }
-    for (; i < t1; i += NT) atomicAdd(&hist[seg_bucket<KK>(__ldcs(src + i), p)], 1u);
+    for (; i < t1; i += NT) atomicAdd(&hist[seg_bucket<KK>(__ldcs(src + i), p, i, B.cuts)], 1u);
     __syncthreads();
     for (int b = threadIdx.x; b < p.k; b += NT) col[(int64_t)b * p.ntiles] = hist[b];
 }
@@ -641,7 +642,8 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *_
             if constexpr (PB != 0) pay[j] = i < nvalid ? __ldcs(sp + r0 + i) : (P)0;
         }
 #pragma unroll
-        for (int j = 0; j < ITEMS; j++) bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p) : -1;
+        for (int j = 0; j < ITEMS; j++)
+            bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts) : -1;
         // count per (bucket, warp): all MATCH.ANY issued back to back, the
         // leaders add with shared atomics on the containing 32-bit word
         unsigned peers[ITEMS];

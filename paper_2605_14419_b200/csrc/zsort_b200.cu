@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/zsort_b200.h"
+#include "dist_kernels.cuh"
 #include "kernels.cuh"
 
 using namespace zsb;
@@ -588,6 +589,7 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     ctx.B.tmp_p = nullptr;
     ctx.B.out_k = (uint64_t *)d_out_keys;
     ctx.B.out_p = d_out_payload;
+    ctx.B.cuts = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0],
@@ -606,6 +608,29 @@ struct ScatterOp {
         if (rc) return rc;
         ZSB_CUDA(cudaStreamSynchronize(c.st));
         return ZSB_OK;
+    }
+};
+
+
+Plan1 plan_partition(int64_t n, int pb, int nparts) {
+    Plan1 P;
+    P.cap = finish_cap(pb);
+    P.half = P.cap / 2;
+    P.k = nparts;
+    int64_t target = (int64_t)num_sms() * 2;
+    int64_t tl = std::max<int64_t>(4096, (n + target - 1) / target);
+    P.tile_len = (tl + 255) & ~(int64_t)255;
+    P.ntiles = (n + P.tile_len - 1) / P.tile_len;
+    return P;
+}
+
+template <int KK, int PB>
+struct PartitionOp {
+    static int run(Ctx &c) {
+        SegParams *seg = (SegParams *)(c.ws + c.L.seg_a);
+        unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+        ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
+        return launch_partition<KK, PB>(c, seg, 1, c.P.ntiles, c.P.k * c.P.ntiles, (int)c.P.k, 2);
     }
 };
 
@@ -677,6 +702,7 @@ int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32
     ctx.B.tmp_p = ctx.ws + ctx.L.tmp_p;
     ctx.B.out_k = (uint64_t *)d_out_keys;
     ctx.B.out_p = d_out_payload;
+    ctx.B.cuts = nullptr;
     return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats);
 }
 
@@ -786,6 +812,137 @@ int zsb_check_sorted(const void *d_in_keys, const void *d_out_keys, const void *
     ZSB_CUDA(cudaMemcpyAsync(&h, viol, 8, cudaMemcpyDeviceToHost, st));
     ZSB_CUDA(cudaStreamSynchronize(st));
     if (h_result) *h_result = (int64_t)h;
+    return ZSB_OK;
+}
+
+
+int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double shift, double *d_out3,
+                      uint64_t *d_out_bits2, void *stream) {
+    int rc = check_common(d_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_dist_init<<<1, 32, 0, st>>>(d_out3, (unsigned long long *)d_out_bits2);
+    ZSB_LAUNCH("k_dist_init");
+    if (n == 0) return ZSB_OK;
+    const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    if (key_dtype == ZSB_KEY_I64)
+        k_local_moments<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, d_out3,
+                                                (unsigned long long *)d_out_bits2);
+    else
+        k_local_moments<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, d_out3,
+                                                (unsigned long long *)d_out_bits2);
+    ZSB_LAUNCH("k_local_moments");
+    return ZSB_OK;
+}
+
+int zsb_bucket_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k,
+                         int64_t *d_counts, void *stream) {
+    int rc = check_common(d_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    if (k < 2 || k > 16384 || !params) return fail(ZSB_ERR_ARG, "need 2 <= k <= 16384 and params");
+    cudaStream_t st = (cudaStream_t)stream;
+    ZSB_CUDA(cudaMemsetAsync(d_counts, 0, (size_t)k * 8, st));
+    if (n == 0) return ZSB_OK;
+    const int grid = std::max(1, std::min<int>(num_sms() * 2, (int)((n + NT - 1) / NT)));
+    const size_t sm = (size_t)k * 4;
+    if (key_dtype == ZSB_KEY_I64) {
+        smem_optin(k_bucket_hist<0>, sm);
+        k_bucket_hist<0><<<grid, NT, sm, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
+                                               (int)k, (unsigned long long *)d_counts);
+    } else {
+        smem_optin(k_bucket_hist<1>, sm);
+        k_bucket_hist<1><<<grid, NT, sm, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
+                                               (int)k, (unsigned long long *)d_counts);
+    }
+    ZSB_LAUNCH("k_bucket_hist");
+    return ZSB_OK;
+}
+
+int zsb_bucket_minmax(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k, int32_t nb,
+                      const int32_t *d_buckets, uint64_t *d_omin, uint64_t *d_omax, void *stream) {
+    int rc = check_common(d_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    if (nb < 0 || nb > 32 || !params) return fail(ZSB_ERR_ARG, "need 0 <= nb <= 32 and params");
+    cudaStream_t st = (cudaStream_t)stream;
+    k_minmax_init<<<1, 32, 0, st>>>(nb, (unsigned long long *)d_omin, (unsigned long long *)d_omax);
+    ZSB_LAUNCH("k_minmax_init");
+    if (n == 0 || nb == 0) return ZSB_OK;
+    const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    if (key_dtype == ZSB_KEY_I64)
+        k_bucket_minmax<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2],
+                                                params[3], (int)k, nb, d_buckets, (unsigned long long *)d_omin,
+                                                (unsigned long long *)d_omax);
+    else
+        k_bucket_minmax<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2],
+                                                params[3], (int)k, nb, d_buckets, (unsigned long long *)d_omin,
+                                                (unsigned long long *)d_omax);
+    ZSB_LAUNCH("k_bucket_minmax");
+    return ZSB_OK;
+}
+
+size_t zsb_partition_workspace_bytes(int64_t n, int32_t payload_bytes, int32_t nparts) {
+    if (n < 1) n = 1;
+    Plan1 P = plan_partition(n, payload_bytes, nparts);
+    return make_layout(n, payload_bytes, P, false).total + align_up(sizeof(DestCuts));
+}
+
+int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes,
+                           int64_t n, const double *params, int64_t k, int64_t gidx_base, int32_t ncuts,
+                           const int32_t *h_cut_bucket, const uint64_t *h_cut_ord, const int64_t *h_cut_gidx,
+                           void *d_out_keys, void *d_out_payload, int64_t *h_part_counts, void *d_workspace,
+                           size_t workspace_bytes, void *stream) {
+    int rc = check_common(d_keys, key_dtype, payload_bytes, n);
+    if (rc) return rc;
+    if (ncuts < 0 || ncuts > MAX_CUTS || !params || k < 2 || k > 16384)
+        return fail(ZSB_ERR_ARG, "need 0 <= ncuts <= 15, 2 <= k <= 16384 and params");
+    const int nparts = ncuts + 1;
+    for (int j = 0; j < nparts; j++) h_part_counts[j] = 0;
+    if (n == 0) return ZSB_OK;
+    Ctx ctx;
+    ctx.n = n;
+    ctx.P = plan_partition(n, payload_bytes, nparts);
+    ctx.L = make_layout(n, payload_bytes, ctx.P, false);
+    const size_t need = ctx.L.total + align_up(sizeof(DestCuts));
+    if (!d_workspace || workspace_bytes < need) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
+    ctx.ws = (unsigned char *)d_workspace;
+    ctx.st = (cudaStream_t)stream;
+    DestCuts hc{};
+    hc.center = params[0];
+    hc.std = params[1];
+    hc.zmin = params[2];
+    hc.scale = params[3];
+    hc.k = (int32_t)k;
+    hc.ncuts = ncuts;
+    hc.gidx_base = gidx_base;
+    for (int j = 0; j < ncuts; j++) {
+        hc.bucket[j] = h_cut_bucket[j];
+        hc.ord[j] = h_cut_ord[j];
+        hc.gidx[j] = h_cut_gidx[j];
+    }
+    DestCuts *dc = (DestCuts *)(ctx.ws + ctx.L.total);
+    ZSB_CUDA(cudaMemcpyAsync(dc, &hc, sizeof(hc), cudaMemcpyHostToDevice, ctx.st));
+    ctx.B.in_k = (const uint64_t *)d_keys;
+    ctx.B.in_p = d_payload;
+    ctx.B.tmp_k = nullptr;
+    ctx.B.tmp_p = nullptr;
+    ctx.B.out_k = (uint64_t *)d_out_keys;
+    ctx.B.out_p = d_out_payload;
+    ctx.B.cuts = dc;
+    SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
+    int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
+    k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, nparts, ctx.P.tile_len, ctx.P.ntiles, 0, 0.0, 1.0,
+                                       0.0, 1.0, MODE_DEST);
+    ZSB_LAUNCH("k_init_level1");
+    rc = dispatch<PartitionOp>(key_dtype, payload_bytes, ctx);
+    if (rc) return rc;
+    // per-destination totals from the scanned matrix: starts at tile 0 of each part
+    std::vector<uint32_t> starts(nparts);
+    const uint32_t *mat = (const uint32_t *)(ctx.ws + ctx.L.mat);
+    ZSB_CUDA(cudaMemcpy2DAsync(starts.data(), sizeof(uint32_t), mat, (size_t)ctx.P.ntiles * 4, sizeof(uint32_t),
+                               nparts, cudaMemcpyDeviceToHost, ctx.st));
+    ZSB_CUDA(cudaStreamSynchronize(ctx.st));
+    for (int j = 0; j < nparts; j++)
+        h_part_counts[j] = (int64_t)((j + 1 < nparts) ? starts[j + 1] : (uint32_t)n) - (int64_t)starts[j];
     return ZSB_OK;
 }
 

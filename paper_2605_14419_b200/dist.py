@@ -1,0 +1,351 @@
+"""Multi-GPU stable z-score partitioning sort (one process per GPU, NCCL).
+
+The reference is single-threaded and has no distributed
+path; this is the B200 extension of its algorithm described in SURVEY.md
+§8(e).  Each rank holds a contiguous shard of the global input (global
+positions [gidx_base, gidx_base + n_local)); the global stable order is
+(key, global position).
+
+  D1  all_reduce of the shard moments (count, sum, sum of squares around a
+      common shift; MIN/MAX of the ordered extremes) -> every rank derives
+      bit-identical fitted z-score parameters (core.py:212-234 with the
+      fitted scale of the single-GPU path);
+  D2  all_gather of the k-bucket z-score histograms -> G-1 cuts at the
+      target positions j*N/G.  A cut falls on a bucket boundary, except
+      inside an all-equal bucket (checked with an all_reduce of per-bucket
+      min/max), where it splits the run by global position -- config 5's
+      10% repeated value is spread over ranks this way;
+  D3  stable partition of every shard by destination rank (the scatter
+      kernel in MODE_DEST, records keep input order) and an NCCL
+      all_to_all_single of keys and payload; chunks arrive in source-rank
+      order, so each rank's received sequence is in global input order;
+  local stable zsort of the received records (the single-GPU path).
+
+The concatenation of the ranks' outputs in rank order is the stable sort of
+the global input.  Local operations are pluggable (`ops`): DeviceOps runs the
+CUDA kernels through the C ABI (the product path); the gloo CPU tests plug in
+numpy stand-ins to exercise the planning and exchange logic without a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as tdist
+
+from . import _lib
+
+SIGN = 1 << 63
+INT64_MIN = -(1 << 63)
+DEFAULT_K = 4096
+
+
+# ------------------------------------------------------------ key images
+
+def ord_to_value(o: int, kind: str) -> float:
+    """Value of the key whose order-preserving image is `o` (as double)."""
+    if kind == "int64":
+        v = (o ^ SIGN)
+        return float(v - (1 << 64) if v >= SIGN else v)
+    b = (o ^ SIGN) if o & SIGN else (~o & ((1 << 64) - 1))
+    return float(np.array([b], np.uint64).view(np.float64)[0])
+
+
+@dataclass(frozen=True)
+class GlobalParams:
+    """Fitted z-score mapping shared by all ranks (same arithmetic everywhere)."""
+
+    center: float
+    std: float
+    zmin: float
+    scale: float
+    k: int
+
+    def as_array(self):
+        return (ctypes.c_double * 4)(self.center, self.std, self.zmin, self.scale)
+
+
+def plan_params(count: float, s1: float, s2: float, shift: float, vmin: float, vmax: float, k: int) -> GlobalParams:
+    """Fitted Eq. 1 parameters from allreduced moments (finalize_params in
+    kernels.cuh, fitted branch).  Degenerate inputs map every key to bucket
+    0, which is still correct (no cut can then fall inside a non-constant
+    bucket), only unbalanced."""
+    mean = shift + s1 / count
+    var = max(0.0, s2 / count - (s1 / count) ** 2)
+    sd = math.sqrt(var)
+    if sd > 0.0 and math.isfinite(sd) and vmax > vmin:
+        span = (vmax - vmin) / sd
+        if span > 0.0 and math.isfinite(span):
+            zmin = (mean - vmin) / sd
+            scale = (k * (1.0 - 2.0 ** -20)) / span
+            if scale > 0.0 and math.isfinite(scale) and math.isfinite(zmin):
+                return GlobalParams(mean, sd, zmin, scale, k)
+    return GlobalParams(0.0, 1.0, 0.0, 1e-300, k)
+
+
+@dataclass(frozen=True)
+class Cut:
+    bucket: int
+    ord: int
+    gidx: int
+
+
+def plan_cuts(counts: np.ndarray, nparts: int, all_equal, occurrence_gidx):
+    """G-1 cuts over the global bucket sequence (SURVEY §8(e) range assignment).
+
+    counts: (G, k) per-rank bucket counts.  all_equal(b) -> (bool, ord) says
+    whether bucket b holds a single key value.  occurrence_gidx(b, t) returns
+    the global index of the t-th record of bucket b in (rank, local) order.
+    """
+    glob = counts.sum(axis=0)
+    total = int(glob.sum())
+    excl = np.concatenate(([0], np.cumsum(glob)))
+    cuts = []
+    for j in range(1, nparts):
+        target = (j * total) // nparts
+        b = int(np.searchsorted(excl, target, side="right") - 1)  # excl[b] <= target < excl[b+1]
+        b = min(max(b, 0), len(glob) - 1) if total else 0
+        if target <= excl[b]:
+            cuts.append(Cut(b, 0, INT64_MIN))
+            continue
+        eq, o = all_equal(b)
+        if eq:
+            t = target - int(excl[b])
+            cuts.append(Cut(b, o, occurrence_gidx(b, t)))
+        else:
+            nxt = b + 1 if (excl[b + 1] - target) < (target - excl[b]) else b
+            cuts.append(Cut(nxt, 0, INT64_MIN))
+    return cuts
+
+
+# ------------------------------------------------------------ local ops
+
+class DeviceOps:
+    """Local work on the rank's GPU through the C ABI (the product path)."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.L = _lib.load()
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    @staticmethod
+    def kind(keys: torch.Tensor) -> str:
+        return "int64" if keys.dtype == torch.int64 else "float64"
+
+    @staticmethod
+    def _kd(keys):
+        return 0 if keys.dtype == torch.int64 else 1
+
+    def local_moments(self, keys: torch.Tensor, shift: float):
+        out = torch.empty(3, dtype=torch.float64, device=self.device)
+        bits = torch.empty(2, dtype=torch.int64, device=self.device)
+        _lib.check(self.L.zsb_local_moments(keys.data_ptr(), self._kd(keys), keys.numel(), float(shift),
+                                            out.data_ptr(), bits.data_ptr(), self._stream()))
+        return out, bits
+
+    def bucket_histogram(self, keys, params: GlobalParams) -> torch.Tensor:
+        c = torch.empty(params.k, dtype=torch.int64, device=self.device)
+        _lib.check(self.L.zsb_bucket_histogram(keys.data_ptr(), self._kd(keys), keys.numel(), params.as_array(),
+                                               params.k, c.data_ptr(), self._stream()))
+        return c
+
+    def bucket_minmax(self, keys, params: GlobalParams, buckets):
+        nb = len(buckets)
+        db = torch.tensor(list(buckets) or [0], dtype=torch.int32, device=self.device)
+        mn = torch.empty(max(nb, 1), dtype=torch.int64, device=self.device)
+        mx = torch.empty(max(nb, 1), dtype=torch.int64, device=self.device)
+        _lib.check(self.L.zsb_bucket_minmax(keys.data_ptr(), self._kd(keys), keys.numel(), params.as_array(), params.k,
+                                            nb, db.data_ptr(), mn.data_ptr(), mx.data_ptr(), self._stream()))
+        return mn[:nb], mx[:nb]
+
+    def occurrence_index(self, keys, key_bits: int, occurrence: int, kind: str) -> int:
+        """Local index of the `occurrence`-th record equal to the key with bits
+        key_bits (for float64, -0.0 and +0.0 are the same key)."""
+        kb = key_bits - (1 << 64) if key_bits >= SIGN else key_bits
+        bits = keys.view(torch.int64)
+        mask = bits == kb
+        if kind == "float64" and key_bits in (0, SIGN):
+            mask |= bits == (INT64_MIN if key_bits == 0 else 0)
+        return int(torch.nonzero(mask)[occurrence].item())
+
+    def partition(self, keys, payload, params: GlobalParams, gidx_base: int, cuts):
+        n = keys.numel()
+        nparts = len(cuts) + 1
+        pb = payload.element_size() if payload is not None else 0
+        ok = torch.empty_like(keys)
+        op = torch.empty_like(payload) if payload is not None else None
+        wsb = self.L.zsb_partition_workspace_bytes(n, pb, nparts)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        cb = (ctypes.c_int32 * max(1, len(cuts)))(*[c.bucket for c in cuts])
+        co = (ctypes.c_uint64 * max(1, len(cuts)))(*[c.ord for c in cuts])
+        cg = (ctypes.c_int64 * max(1, len(cuts)))(*[c.gidx for c in cuts])
+        counts = (ctypes.c_int64 * nparts)()
+        _lib.check(self.L.zsb_partition_to_ranks(keys.data_ptr(), self._kd(keys),
+                                                 payload.data_ptr() if payload is not None else None, pb, n,
+                                                 params.as_array(), params.k, int(gidx_base), len(cuts), cb, co, cg,
+                                                 ok.data_ptr(), op.data_ptr() if op is not None else None, counts,
+                                                 ws.data_ptr(), wsb, self._stream()))
+        return ok, op, [int(x) for x in counts]
+
+    def local_sort(self, keys, payload):
+        from .core import zsort
+        k, p, _ = zsort(keys, payload)
+        return k, p
+
+
+# ------------------------------------------------------------- comms
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    _OPS = {"sum": tdist.ReduceOp.SUM, "min": tdist.ReduceOp.MIN, "max": tdist.ReduceOp.MAX}
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = tdist.get_world_size(group) if tdist.is_initialized() else 1
+        self.rank = tdist.get_rank(group) if tdist.is_initialized() else 0
+
+    def all_reduce(self, t: torch.Tensor, op: str) -> torch.Tensor:
+        if self.world > 1:
+            tdist.all_reduce(t, op=self._OPS[op], group=self.group)
+        return t
+
+    def all_gather(self, t: torch.Tensor):
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        tdist.all_gather(out, t, group=self.group)
+        return out
+
+    def all_to_all_single(self, out, inp, out_splits=None, in_splits=None):
+        tdist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                group=self.group)
+
+
+# ------------------------------------------------------------- the sort
+
+def dist_zsort(keys: torch.Tensor, payload: torch.Tensor | None, gidx_base: int, group=None, ops=None,
+               k: int = DEFAULT_K, comm=None):
+    """Globally stable sort of sharded records; returns this rank's slice.
+
+    keys/payload: this rank's shard (contiguous global positions starting at
+    gidx_base).  Returns (keys, payload, info) where concatenating every
+    rank's result in rank order gives the stable sort of the global input.
+    """
+    ops = ops or DeviceOps(keys.device)
+    comm = comm or TorchComm(group)
+    world, rank = comm.world, comm.rank
+    dev = ops.device
+    kind = ops.kind(keys)
+    n = keys.numel()
+    info = {"world": world}
+
+    # ---- D1: extremes, then shifted moments (two tiny all_reduces)
+    _, bits = ops.local_moments(keys, 0.0)
+    mn = torch.tensor([bits[0].item() if n else -1], dtype=torch.int64, device=dev)  # as signed for MIN/MAX
+    mx = torch.tensor([bits[1].item() if n else 0], dtype=torch.int64, device=dev)
+    # ordered images are unsigned; flip the sign bit so signed MIN/MAX order them
+    mn ^= INT64_MIN
+    mx ^= INT64_MIN
+    if n == 0:
+        mn.fill_(2**63 - 1)
+        mx.fill_(INT64_MIN)
+    comm.all_reduce(mn, "min")
+    comm.all_reduce(mx, "max")
+    omin = (int(mn.item()) ^ INT64_MIN) & ((1 << 64) - 1)
+    omax = (int(mx.item()) ^ INT64_MIN) & ((1 << 64) - 1)
+    vmin, vmax = ord_to_value(omin, kind), ord_to_value(omax, kind)
+    shift = 0.5 * vmin + 0.5 * vmax
+    mom, _ = ops.local_moments(keys, shift)
+    mom = mom.clone()
+    comm.all_reduce(mom, "sum")
+    count, s1, s2 = (float(x) for x in mom.tolist())
+    info.update(total=int(count), omin=omin, omax=omax)
+    if count == 0:
+        return keys.clone(), (payload.clone() if payload is not None else None), info
+    if omin == omax or world == 1:  # globally constant (already stable) or nothing to exchange
+        k_, p_ = ops.local_sort(keys, payload) if n else (keys.clone(), payload)
+        return k_, p_, info
+    params = plan_params(count, s1, s2, shift, vmin, vmax, k)
+
+    # ---- D2: per-rank histograms (all_gather) -> cuts
+    hist = ops.bucket_histogram(keys, params)
+    gathered = comm.all_gather(hist)
+    counts = torch.stack(gathered).cpu().numpy()
+    glob = counts.sum(axis=0)
+    excl = np.concatenate(([0], np.cumsum(glob)))
+    total = int(glob.sum())
+    inside = []
+    for j in range(1, world):
+        target = (j * total) // world
+        b = int(np.searchsorted(excl, target, side="right") - 1)
+        if excl[b] < target:
+            inside.append(b)
+    inside = sorted(set(inside))
+    eq = {}
+    if inside:
+        bmn, bmx = ops.bucket_minmax(keys, params, inside)
+        bmn = (bmn ^ INT64_MIN).clone()
+        bmx = (bmx ^ INT64_MIN).clone()
+        comm.all_reduce(bmn, "min")
+        comm.all_reduce(bmx, "max")
+        for b, a, z in zip(inside, bmn.tolist(), bmx.tolist()):
+            a = (a ^ INT64_MIN) & ((1 << 64) - 1)
+            z = (z ^ INT64_MIN) & ((1 << 64) - 1)
+            eq[b] = (a == z, a)
+    # global index of an occurrence inside an all-equal bucket: owner rank answers
+    requests = []
+
+    def all_equal(b):
+        return eq.get(b, (False, 0))
+
+    def occurrence_gidx(b, t):
+        requests.append((b, t))
+        return len(requests) - 1  # placeholder, resolved below
+
+    cuts = plan_cuts(counts, world, all_equal, occurrence_gidx)
+    if requests:
+        answers = torch.full((len(requests),), INT64_MIN, dtype=torch.int64, device=dev)
+        for q, (b, t) in enumerate(requests):
+            before = 0
+            for r in range(world):
+                c = int(counts[r][b])
+                if before <= t < before + c:
+                    if r == rank:
+                        value_bits = _ord_to_bits(eq[b][1], kind)
+                        answers[q] = gidx_base + ops.occurrence_index(keys, value_bits, t - before, kind)
+                    break
+                before += c
+        comm.all_reduce(answers, "max")
+        ans = answers.tolist()
+        cuts = [Cut(c.bucket, c.ord, ans[c.gidx]) if c.gidx != INT64_MIN else c for c in cuts]
+    info["cuts"] = cuts
+
+    # ---- D3: stable partition by destination, all_to_all of keys and payload
+    pk, pp, send = ops.partition(keys, payload, params, gidx_base, cuts)
+    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+    recv_t = torch.empty_like(send_t)
+    comm.all_to_all_single(recv_t, send_t)
+    recv = [int(x) for x in recv_t.tolist()]
+    rk = torch.empty(sum(recv), dtype=keys.dtype, device=dev)
+    comm.all_to_all_single(rk, pk, recv, send)
+    rp = None
+    if payload is not None:
+        rp = torch.empty(sum(recv), dtype=payload.dtype, device=dev)
+        comm.all_to_all_single(rp, pp, recv, send)
+    info.update(sent=send, received=recv)
+    # ---- local stable sort of the received records (global input order)
+    if rk.numel() == 0:
+        return rk, rp, info
+    ok, op = ops.local_sort(rk, rp)
+    return ok, op, info
+
+
+def _ord_to_bits(o: int, kind: str) -> int:
+    if kind == "int64":
+        return o ^ SIGN
+    return (o ^ SIGN) if o & SIGN else (~o & ((1 << 64) - 1))
