@@ -192,6 +192,7 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+        return run_dist(args, rank, world, dev)
     L = _lib.load()
     keys_h, pay_h = make_workload(args.config, rank, world)
     n = keys_h.size
@@ -325,6 +326,85 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_dist(args, rank, world, dev):
+    """N > 1: weak scaling of the globally stable sort over NCCL (dist.py).
+
+    Each rank owns a shard of the config-2 recipe (10^7 float64 N(0,1) keys,
+    seed 1 + rank, int32 global-index payload); the global input is the
+    concatenation of the shards in rank order.  One step = D1 allreduce, D2
+    allgather, stable partition, NCCL all-to-all, local stable sort.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_14419_b200.dist import dist_zsort
+
+    n = 10**7 if args.config == 2 else 10**6
+    keys_h = np.random.default_rng(1 + rank).standard_normal(n)
+    pay_h = np.arange(rank * n, (rank + 1) * n, dtype=np.int32)
+    dk = torch.from_numpy(keys_h).to(dev)
+    dp = torch.from_numpy(pay_h).to(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        ok, op, info = dist_zsort(dk, dp, rank * n)
+    torch.cuda.synchronize()
+    step_ms = []
+    with ClockSampler(dev.index) as clk:
+        t_end = time.perf_counter() + 1.5
+        while time.perf_counter() < t_end:
+            dist_zsort(dk, dp, rank * n)
+        for _ in range(args.steps):
+            flush.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ok, op, info = dist_zsort(dk, dp, rank * n)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        dist.barrier()
+    t = torch.tensor([sum(step_ms)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    # e2e: pinned host shard -> device -> distributed sort -> pinned host result
+    hk = torch.from_numpy(keys_h).pin_memory()
+    hp = torch.from_numpy(pay_h).pin_memory()
+    e2e = []
+    for _ in range(3):
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        k_, p_, _ = dist_zsort(hk.to(dev, non_blocking=True), hp.to(dev, non_blocking=True), rank * n)
+        rk, rp = k_.cpu(), p_.cpu()
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+    te = torch.tensor([sum(e2e) / len(e2e)], device=dev, dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        hbm_peak, peak_kind = peaks()
+        line = {
+            "metric": METRIC, "value": n * world / (ms_per_step / 1e3), "unit": "keys/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 recipe sharded: {n} float64 N(0,1) keys per GPU (seed 1+rank), int32 "
+                                   f"global-index payload; globally stable sort", "n_per_gpu": n,
+                       "parallelism": f"dp{world} (D1 allreduce, D2 allgather, NCCL all_to_all exchange)",
+                       "l2": "flushed (512 MiB write) between timed steps"},
+            "sort_roofline": {"alg_bytes_per_key": 64 + 2 * 12, "note": "local sort 64 B/key + partition 24 B/key"},
+            "exchange": {"sent_per_rank": info.get("sent"), "received_rank0": info.get("received")},
+            "e2e": {"value": n * world / (float(te.item()) / 1e3), "unit": "keys/s",
+                    "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * 12)},
+            "gpu_launches": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

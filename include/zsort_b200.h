@@ -144,6 +144,15 @@ int zsb_bucket_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const
 int zsb_bucket_minmax(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k, int32_t nb,
                       const int32_t *d_buckets, uint64_t *d_omin, uint64_t *d_omax, void *stream);
 
+/* Refinement histograms for a cut that falls inside a bucket: for each of
+ * nq (<= 32) queries, counts the local records with bucket == d_qbucket[q]
+ * and ordered key in [d_qlo[q], d_qhi[q]] by the exact digit
+ * (ord - d_qlo[q]) >> d_qshift[q] into d_counts[q*nbins + digit] (int64,
+ * zeroed by the call). */
+int zsb_range_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k, int32_t nq,
+                        const int32_t *d_qbucket, const uint64_t *d_qlo, const uint64_t *d_qhi, const int32_t *d_qshift,
+                        int32_t nbins, int64_t *d_counts, void *stream);
+
 /* D3 input: stable partition of the local shard into ncuts+1 destination
  * ranks.  Record i (global index gidx_base + i) goes to the number of cuts
  * c_j with (bucket(x), ord(x), gidx) >= (h_cut_bucket[j], h_cut_ord[j],

@@ -38,7 +38,7 @@ EXPORTS = (
     "zsb_check_workspace_bytes", "zsb_check_sorted", "zsb_last_error", "zsb_version",
     "zsb_timing_enable", "zsb_timing_read",
     "zsb_local_moments", "zsb_bucket_histogram", "zsb_bucket_minmax", "zsb_partition_workspace_bytes",
-    "zsb_partition_to_ranks",
+    "zsb_partition_to_ranks", "zsb_range_histogram",
 )
 
 PHASES = ("moments", "histogram", "scan", "scatter", "classify", "finish", "recursion_stats", "misc")
@@ -80,6 +80,8 @@ def load(auto_build: bool = True):
     L.zsb_bucket_histogram.restype = ctypes.c_int
     L.zsb_bucket_minmax.argtypes = [P, I32, I64, P, I64, I32, P, P, P, P]
     L.zsb_bucket_minmax.restype = ctypes.c_int
+    L.zsb_range_histogram.argtypes = [P, I32, I64, P, I64, I32, P, P, P, P, I32, P, P]
+    L.zsb_range_histogram.restype = ctypes.c_int
     L.zsb_partition_workspace_bytes.argtypes = [I64, I32, I32]
     L.zsb_partition_workspace_bytes.restype = SZ
     L.zsb_partition_to_ranks.argtypes = [P, I32, P, I32, I64, P, I64, I64, I32, P, P, P, P, P, P, P, SZ, P]

@@ -83,6 +83,28 @@ __global__ void __launch_bounds__(NT) k_bucket_minmax(const uint64_t *__restrict
     }
 }
 
+// Refinement histograms for cuts inside a bucket: query q counts the local
+// records with bucket == qb[q] and ordered key in [qlo[q], qhi[q]] by the
+// exact digit (ord - qlo) >> qsh[q] (nbins bins per query).
+template <int KK>
+__global__ void __launch_bounds__(NT) k_range_hist(const uint64_t *__restrict__ keys, int64_t n, double center,
+                                                   double sd, double zmin, double scale, int k, int nq,
+                                                   const int32_t *__restrict__ qb, const uint64_t *__restrict__ qlo,
+                                                   const uint64_t *__restrict__ qhi, const int32_t *__restrict__ qsh,
+                                                   int nbins, unsigned long long *counts) {
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+        const uint64_t b = __ldcs(keys + i);
+        const int bk = bucket_z(key_value<KK>(b), center, sd, zmin, scale, k);
+        const uint64_t o = ord_key<KK>(b);
+        for (int q = 0; q < nq; q++) {
+            if (bk == qb[q] && o >= qlo[q] && o <= qhi[q]) {
+                const uint64_t d = (o - qlo[q]) >> qsh[q];
+                if (d < (uint64_t)nbins) atomicAdd(&counts[(int64_t)q * nbins + d], 1ull);
+            }
+        }
+    }
+}
+
 __global__ void k_minmax_init(int nb, unsigned long long *omin, unsigned long long *omax) {
     if ((int)threadIdx.x < nb) {
         omin[threadIdx.x] = ~0ull;

@@ -880,6 +880,28 @@ int zsb_bucket_minmax(const void *d_keys, int32_t key_dtype, int64_t n, const do
     return ZSB_OK;
 }
 
+int zsb_range_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double *params, int64_t k, int32_t nq,
+                        const int32_t *d_qbucket, const uint64_t *d_qlo, const uint64_t *d_qhi, const int32_t *d_qshift,
+                        int32_t nbins, int64_t *d_counts, void *stream) {
+    int rc = check_common(d_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    if (nq < 0 || nq > 32 || nbins < 1 || nbins > 65536 || !params) return fail(ZSB_ERR_ARG, "bad range query");
+    cudaStream_t st = (cudaStream_t)stream;
+    ZSB_CUDA(cudaMemsetAsync(d_counts, 0, (size_t)nq * nbins * 8, st));
+    if (n == 0 || nq == 0) return ZSB_OK;
+    const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    if (key_dtype == ZSB_KEY_I64)
+        k_range_hist<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
+                                             (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
+                                             (unsigned long long *)d_counts);
+    else
+        k_range_hist<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
+                                             (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
+                                             (unsigned long long *)d_counts);
+    ZSB_LAUNCH("k_range_hist");
+    return ZSB_OK;
+}
+
 size_t zsb_partition_workspace_bytes(int64_t n, int32_t payload_bytes, int32_t nparts) {
     if (n < 1) n = 1;
     Plan1 P = plan_partition(n, payload_bytes, nparts);

@@ -122,6 +122,94 @@ def plan_cuts(counts: np.ndarray, nparts: int, all_equal, occurrence_gidx):
     return cuts
 
 
+REFINE_BITS = 12
+
+
+def plan_cuts_exact(counts, world, rank, keys, params, gidx_base, ops, comm, kind):
+    """Exact G-1 cuts at the target positions j*N/G of the global stable order.
+
+    A target on a bucket boundary cuts there.  A target inside bucket B is
+    refined with exact integer-digit histograms of B's ordered key range
+    (REFINE_BITS per round, batched over targets, one all_gather each) until
+    it lands on a key boundary -- a key-level cut -- or on a single key value,
+    whose run is then cut by global position (the record at that position is
+    found by the rank that owns it).  Every rank computes identical cuts.
+    """
+    dev = ops.device
+    glob = counts.sum(axis=0)
+    total = int(glob.sum())
+    excl = np.concatenate(([0], np.cumsum(glob)))
+    cuts = [None] * (world - 1)
+    pending = []  # [j, bucket, t (offset inside the current range), lo, hi, per-rank counts]
+    for j in range(1, world):
+        target = (j * total) // world
+        b = int(np.searchsorted(excl, target, side="right") - 1)
+        b = min(max(b, 0), len(glob) - 1)
+        if target <= excl[b]:
+            cuts[j - 1] = Cut(b, 0, INT64_MIN)
+        else:
+            pending.append([j, b, int(target - excl[b]), None, None, counts[:, b].astype(np.int64)])
+    if pending:
+        bs = sorted({q[1] for q in pending})
+        bmn, bmx = ops.bucket_minmax(keys, params, bs)
+        bmn = (bmn ^ INT64_MIN).clone()
+        bmx = (bmx ^ INT64_MIN).clone()
+        comm.all_reduce(bmn, "min")
+        comm.all_reduce(bmx, "max")
+        ext = {b: ((a ^ INT64_MIN) & MASK64, (z ^ INT64_MIN) & MASK64) for b, a, z in zip(bs, bmn.tolist(), bmx.tolist())}
+        for q in pending:
+            q[3], q[4] = ext[q[1]]
+    requests = []
+    for _round in range(64 // REFINE_BITS + 3):
+        active = []
+        for q in pending:
+            if cuts[q[0] - 1] is not None:
+                continue
+            if q[3] == q[4]:  # one key value: cut its run by global position
+                requests.append(q)
+                cuts[q[0] - 1] = "pos"
+            else:
+                active.append(q)
+        if not active:
+            break
+        shifts = [max(0, (q[4] - q[3]).bit_length() - REFINE_BITS) for q in active]
+        nbins = 1 << REFINE_BITS
+        h = ops.range_histogram(keys, params, [q[1] for q in active], [q[3] for q in active],
+                                [q[4] for q in active], shifts, nbins)
+        allh = torch.stack(comm.all_gather(h)).cpu().numpy().reshape(world, len(active), nbins)
+        for qi, (q, sh) in enumerate(zip(active, shifts)):
+            g = allh[:, qi, :].sum(axis=0)
+            ex = np.concatenate(([0], np.cumsum(g)))
+            d = int(np.searchsorted(ex, q[2], side="right") - 1)
+            if q[2] == ex[d]:  # on a key boundary: records with ord >= that key go right
+                cuts[q[0] - 1] = Cut(q[1], q[3] + (d << sh), INT64_MIN)
+            else:
+                q[2] -= int(ex[d])
+                lo = q[3] + (d << sh)
+                q[3], q[4] = lo, min(q[4], lo + (1 << sh) - 1)
+                q[5] = allh[:, qi, d].astype(np.int64)
+    if requests:
+        answers = torch.full((len(requests),), INT64_MIN, dtype=torch.int64, device=dev)
+        for qi, q in enumerate(requests):
+            before = 0
+            for r in range(world):
+                c = int(q[5][r])
+                if before <= q[2] < before + c:
+                    if r == rank:
+                        answers[qi] = gidx_base + ops.occurrence_index(keys, _ord_to_bits(q[3], kind), q[2] - before,
+                                                                      kind)
+                    break
+                before += c
+        comm.all_reduce(answers, "max")
+        for q, g in zip(requests, answers.tolist()):
+            cuts[q[0] - 1] = Cut(q[1], q[3], int(g))
+    assert all(isinstance(c, Cut) for c in cuts), cuts
+    return cuts
+
+
+MASK64 = (1 << 64) - 1
+
+
 # ------------------------------------------------------------ local ops
 
 class DeviceOps:
@@ -163,6 +251,18 @@ class DeviceOps:
         _lib.check(self.L.zsb_bucket_minmax(keys.data_ptr(), self._kd(keys), keys.numel(), params.as_array(), params.k,
                                             nb, db.data_ptr(), mn.data_ptr(), mx.data_ptr(), self._stream()))
         return mn[:nb], mx[:nb]
+
+    def range_histogram(self, keys, params: GlobalParams, buckets, lo, hi, shifts, nbins):
+        nq = len(buckets)
+        qb = torch.tensor(buckets, dtype=torch.int32, device=self.device)
+        qlo = torch.tensor([x - (1 << 64) if x >= SIGN else x for x in lo], dtype=torch.int64, device=self.device)
+        qhi = torch.tensor([x - (1 << 64) if x >= SIGN else x for x in hi], dtype=torch.int64, device=self.device)
+        qs = torch.tensor(shifts, dtype=torch.int32, device=self.device)
+        c = torch.empty(nq * nbins, dtype=torch.int64, device=self.device)
+        _lib.check(self.L.zsb_range_histogram(keys.data_ptr(), self._kd(keys), keys.numel(), params.as_array(),
+                                              params.k, nq, qb.data_ptr(), qlo.data_ptr(), qhi.data_ptr(),
+                                              qs.data_ptr(), nbins, c.data_ptr(), self._stream()))
+        return c
 
     def occurrence_index(self, keys, key_bits: int, occurrence: int, kind: str) -> int:
         """Local index of the `occurrence`-th record equal to the key with bits
@@ -274,55 +374,8 @@ def dist_zsort(keys: torch.Tensor, payload: torch.Tensor | None, gidx_base: int,
 
     # ---- D2: per-rank histograms (all_gather) -> cuts
     hist = ops.bucket_histogram(keys, params)
-    gathered = comm.all_gather(hist)
-    counts = torch.stack(gathered).cpu().numpy()
-    glob = counts.sum(axis=0)
-    excl = np.concatenate(([0], np.cumsum(glob)))
-    total = int(glob.sum())
-    inside = []
-    for j in range(1, world):
-        target = (j * total) // world
-        b = int(np.searchsorted(excl, target, side="right") - 1)
-        if excl[b] < target:
-            inside.append(b)
-    inside = sorted(set(inside))
-    eq = {}
-    if inside:
-        bmn, bmx = ops.bucket_minmax(keys, params, inside)
-        bmn = (bmn ^ INT64_MIN).clone()
-        bmx = (bmx ^ INT64_MIN).clone()
-        comm.all_reduce(bmn, "min")
-        comm.all_reduce(bmx, "max")
-        for b, a, z in zip(inside, bmn.tolist(), bmx.tolist()):
-            a = (a ^ INT64_MIN) & ((1 << 64) - 1)
-            z = (z ^ INT64_MIN) & ((1 << 64) - 1)
-            eq[b] = (a == z, a)
-    # global index of an occurrence inside an all-equal bucket: owner rank answers
-    requests = []
-
-    def all_equal(b):
-        return eq.get(b, (False, 0))
-
-    def occurrence_gidx(b, t):
-        requests.append((b, t))
-        return len(requests) - 1  # placeholder, resolved below
-
-    cuts = plan_cuts(counts, world, all_equal, occurrence_gidx)
-    if requests:
-        answers = torch.full((len(requests),), INT64_MIN, dtype=torch.int64, device=dev)
-        for q, (b, t) in enumerate(requests):
-            before = 0
-            for r in range(world):
-                c = int(counts[r][b])
-                if before <= t < before + c:
-                    if r == rank:
-                        value_bits = _ord_to_bits(eq[b][1], kind)
-                        answers[q] = gidx_base + ops.occurrence_index(keys, value_bits, t - before, kind)
-                    break
-                before += c
-        comm.all_reduce(answers, "max")
-        ans = answers.tolist()
-        cuts = [Cut(c.bucket, c.ord, ans[c.gidx]) if c.gidx != INT64_MIN else c for c in cuts]
+    counts = torch.stack(comm.all_gather(hist)).cpu().numpy()  # (G, k)
+    cuts = plan_cuts_exact(counts, world, rank, keys, params, gidx_base, ops, comm, kind)
     info["cuts"] = cuts
 
     # ---- D3: stable partition by destination, all_to_all of keys and payload

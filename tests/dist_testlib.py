@@ -101,6 +101,16 @@ class NumpyOps:
         return (torch.tensor(np.array(mn, np.uint64).view(np.int64)),
                 torch.tensor(np.array(mx, np.uint64).view(np.int64)))
 
+    def range_histogram(self, keys, params, buckets, lo, hi, shifts, nbins):
+        ids = self.bucket_ids(keys, params)
+        o = O.ordered_u64(keys.numpy())
+        out = np.zeros((len(buckets), nbins), np.int64)
+        for q, (b, a, z, sh) in enumerate(zip(buckets, lo, hi, shifts)):
+            sel = o[(ids == b) & (o >= np.uint64(a)) & (o <= np.uint64(z))]
+            d = ((sel - np.uint64(a)) >> np.uint64(sh)).astype(np.int64)
+            out[q] = np.bincount(d, minlength=nbins)[:nbins]
+        return torch.from_numpy(out.reshape(-1))
+
     def occurrence_index(self, keys, key_bits, occurrence, kind):
         o = O.ordered_u64(keys.numpy())
         target = O.ordered_u64(np.array([key_bits], np.uint64).view(np.int64 if kind == "int64" else np.float64))[0]
