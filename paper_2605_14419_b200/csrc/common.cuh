@@ -22,6 +22,8 @@ enum SegMode : int32_t {
     MODE_INTEGER = 1,  // exact MSD digit of (ord(key) - ord(min)): termination fallback (K7)
     MODE_COPY = 2,     // all keys equal: copy through (core.py:377-380, _kernels.py:339-343)
     MODE_DEST = 3,     // multi-GPU exchange: bucket = destination rank from the global cuts
+    MODE_ZCDF = 4,     // level 1, fitted: z-score coordinate through the piecewise-linear empirical CDF
+                       // (histogram equalisation over kf coarse z-bins) -> equal-population buckets
 };
 
 // Global cuts of the multi-GPU exchange (paper_2605_14419_b200/dist.py).
@@ -61,6 +63,8 @@ struct SegParams {
     int32_t level;     // partition depth (1 = first level)
     int32_t shift;     // integer mode: digit = (ord - umin) >> shift
     int32_t src;       // buffer holding the segment: 0 = input, 1 = tmp, 2 = out
+    int32_t kf;        // MODE_ZCDF: coarse z-bins of the CDF table (scale is the coarse scale)
+    int32_t pad;
 };
 
 // Per-segment accumulator for the recursion moments pass (fused_stats_pass,
@@ -156,9 +160,38 @@ __device__ __forceinline__ int32_t dest_of(uint64_t bits, int64_t pos, const Des
     return d;
 }
 
+// Histogram-equalised z-score bucket: h = Eq. 1 coordinate over kf coarse
+// z-bins (unfloored); within coarse bin s the bucket interpolates the
+// empirical CDF linearly, cdf[s] .. cdf[s+1] (cdf in bucket units, cdf[0] = 0,
+// cdf[kf] = k).  Clamping each bin to [floor(cdf[s]), floor(cdf[s+1])] keeps
+// the map monotone in the key under any rounding.
+__device__ __forceinline__ int32_t bucket_cdf(double x, const SegParams &p, const double *cdf) {
+    const double h = __dmul_rn(__dadd_rn(__ddiv_rn(__dsub_rn(x, p.center), p.std), p.zmin), p.scale);
+    double fs = floor(h);
+    int s;
+    double fr;
+    if (!(fs > 0.0)) {
+        s = 0;
+        fr = h > 0.0 ? h : 0.0;
+    } else if (fs >= (double)p.kf) {
+        s = p.kf - 1;
+        fr = 1.0;
+    } else {
+        s = (int)fs;
+        fr = h - fs;
+    }
+    const double a = cdf[s], z = cdf[s + 1];
+    const double lo = floor(a), hi = floor(z);
+    double b = floor(__dadd_rn(a, __dmul_rn(fr, __dsub_rn(z, a))));
+    b = b < lo ? lo : (b > hi ? hi : b);
+    const int bi = (int)b;
+    return bi < p.k ? bi : p.k - 1;
+}
+
 template <int KK>
 __device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p, int64_t pos = 0,
-                                              const DestCuts *cuts = nullptr) {
+                                              const DestCuts *cuts = nullptr, const double *cdf = nullptr) {
+    if (p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
     if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
     if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
     if (p.mode == MODE_DEST) return dest_of<KK>(bits, pos, cuts);

@@ -30,6 +30,7 @@ struct Buffers {
     uint64_t *out_k;
     void *out_p;
     const DestCuts *cuts;  // MODE_DEST only
+    const double *cdf;     // MODE_ZCDF only: kf + 1 CDF knots in bucket units (global; staged in smem)
 };
 
 __device__ __forceinline__ const uint64_t *src_keys(const Buffers &B, int src) {
@@ -380,8 +381,10 @@ __global__ void k_seg_params(SegParams *segs, int nseg, const SegAcc *acc, MapCf
 
 // ------------------------------------------------------------------- K2
 
+constexpr int HT = 1024;  // threads of the histogram kernel (one tile per CTA)
+
 template <int KK>
-__global__ void __launch_bounds__(NT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
+__global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
                                              uint32_t *__restrict__ mat) {
     extern __shared__ uint32_t hist[];
     int s = find_seg(segs, nseg, blockIdx.x);
@@ -391,23 +394,26 @@ __global__ void __launch_bounds__(NT) k_hist(Buffers B, const SegParams *__restr
     int64_t t1 = min(t0 + p.tile_len, p.start + p.len);
     uint32_t *col = mat + p.mat_base + ti;
     if (p.mode == MODE_COPY) {  // one bucket holds the whole tile
-        for (int b = threadIdx.x; b < p.k; b += NT) col[(int64_t)b * p.ntiles] = b == 0 ? (uint32_t)(t1 - t0) : 0u;
+        for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = b == 0 ? (uint32_t)(t1 - t0) : 0u;
         return;
     }
-    for (int b = threadIdx.x; b < p.k; b += NT) hist[b] = 0;
+    for (int b = threadIdx.x; b < p.k; b += HT) hist[b] = 0;
+    double *cdf = (double *)(hist + ((p.k + 1) & ~1));
+    if (p.mode == MODE_ZCDF)
+        for (int q = threadIdx.x; q <= p.kf; q += HT) cdf[q] = B.cdf[q];
     __syncthreads();
     const uint64_t *src = src_keys(B, p.src);
     int64_t i = t0 + threadIdx.x;
-    for (; i + 7 * NT < t1; i += 8 * NT) {
+    for (; i + 7 * HT < t1; i += 8 * HT) {
         uint64_t b[8];
 #pragma unroll
-        for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * NT);
+        for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
 #pragma unroll
-        for (int u = 0; u < 8; u++) atomicAdd(&hist[seg_bucket<KK>(b[u], p, i + u * NT, B.cuts)], 1u);
+        for (int u = 0; u < 8; u++) atomicAdd(&hist[seg_bucket<KK>(b[u], p, i + u * HT, B.cuts, cdf)], 1u);
     }
-    for (; i < t1; i += NT) atomicAdd(&hist[seg_bucket<KK>(__ldcs(src + i), p, i, B.cuts)], 1u);
+    for (; i < t1; i += HT) atomicAdd(&hist[seg_bucket<KK>(__ldcs(src + i), p, i, B.cuts, cdf)], 1u);
     __syncthreads();
-    for (int b = threadIdx.x; b < p.k; b += NT) col[(int64_t)b * p.ntiles] = hist[b];
+    for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
 }
 
 // ------------------------------------------------------------------- K3
@@ -513,52 +519,65 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 // serialization.
 
 constexpr int SCAT_ITEMS = 16;
-constexpr int SCAT_ROUND = NT * SCAT_ITEMS;  // 4096 records per round
-constexpr int KSCAT_MAX = 2048;             // fan-out limit of one pass
+constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
+// SW warps per CTA: 8 (4096-record rounds, two CTAs per SM) for k <= 1024,
+// 16 (8192-record rounds, one CTA per SM) above, so that a bucket's run in a
+// round stays >= 4 records = one 32-byte sector of keys (shorter runs leave
+// partially written sectors that cost a DRAM read-modify-write).
+inline int scat_warps(int k, int threshold = 1024) { return k <= threshold ? 8 : 16; }
+
+constexpr int CDF_KNOTS = 1024;  // coarse z-bins of the level-1 equalisation table
 
 struct ScatLayout {
-    size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, total;
+    size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, off_cdf, total;
 };
 
-__host__ __device__ inline ScatLayout scat_layout(int k, int pb) {
+__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
+    const int round = sw * 32 * SCAT_ITEMS;
     ScatLayout L;
     size_t o = 0;
     L.off_cur = o;
     o += (size_t)k * 4;
     o = (o + 15) & ~(size_t)15;
     L.off_cnt = o;
-    o += (size_t)k * NWARPS * 2;
+    o += (size_t)k * sw * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_lst = o;
     o += (size_t)(k + 1) * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_k = o;
-    o += (size_t)SCAT_ROUND * 8;
+    o += (size_t)round * 8;
     L.off_p = o;
-    o += (size_t)SCAT_ROUND * pb;
+    o += (size_t)round * pb;
     o = (o + 15) & ~(size_t)15;
     L.off_b = o;
-    o += (size_t)SCAT_ROUND * 2;
-    L.total = (o + 15) & ~(size_t)15;
+    o += (size_t)round * 2;
+    o = (o + 15) & ~(size_t)15;
+    L.off_cdf = o;  // the CDF table (level-1 equalisation only) follows the layout
+    L.total = o;
     return L;
 }
 
 // Exclusive scan, in (digit, warp) order, of per-(digit, warp) u16 counters
-// laid out [digit][NWARPS] (one uint4 per digit).  Thread t owns digits
+// laid out [digit][SW] (SW/8 uint4 per digit).  Thread t owns digits
 // [t*per, (t+1)*per): a thread-local pass over its uint4s, one block scan
 // of the thread totals, and a write-back pass.  Also writes the digit
 // starts to dstart[0..ndig] (dstart[ndig] = total).  Ends with a barrier.
-__device__ __forceinline__ void scan_dw8(uint16_t *cnt, int ndig, uint16_t *dstart, uint32_t *wsum) {
-    static_assert(NWARPS == 8, "one uint4 per digit");
+template <int SW>
+__device__ __forceinline__ void scan_dw(uint16_t *cnt, int ndig, uint16_t *dstart, uint32_t *wsum) {
+    constexpr int T = SW * 32, V = SW / 8;
     const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-    const int per = (ndig + NT - 1) / NT;
+    const int per = (ndig + T - 1) / T;
     const int d0 = min(ndig, tid * per), d1 = min(ndig, d0 + per);
     uint4 *c4 = (uint4 *)cnt;
     uint32_t tsum = 0;
     for (int d = d0; d < d1; d++) {
-        const uint4 v = c4[d];
-        tsum += (v.x & 0xffff) + (v.x >> 16) + (v.y & 0xffff) + (v.y >> 16) + (v.z & 0xffff) + (v.z >> 16) +
-                (v.w & 0xffff) + (v.w >> 16);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            const uint4 x = c4[d * V + v];
+            tsum += (x.x & 0xffff) + (x.x >> 16) + (x.y & 0xffff) + (x.y >> 16) + (x.z & 0xffff) + (x.z >> 16) +
+                    (x.w & 0xffff) + (x.w >> 16);
+        }
     }
     uint32_t x = tsum;
 #pragma unroll
@@ -571,29 +590,45 @@ __device__ __forceinline__ void scan_dw8(uint16_t *cnt, int ndig, uint16_t *dsta
     uint32_t run = x - tsum;
     for (int q = 0; q < w; q++) run += wsum[q];
     for (int d = d0; d < d1; d++) {
-        const uint4 v = c4[d];
         dstart[d] = (uint16_t)run;
-        uint32_t h[8] = {v.x & 0xffff, v.x >> 16, v.y & 0xffff, v.y >> 16,
-                         v.z & 0xffff, v.z >> 16, v.w & 0xffff, v.w >> 16};
-        uint32_t e[8];
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-            e[q] = run;
-            run += h[q];
+        for (int v = 0; v < V; v++) {
+            const uint4 xv = c4[d * V + v];
+            uint32_t h[8] = {xv.x & 0xffff, xv.x >> 16, xv.y & 0xffff, xv.y >> 16,
+                             xv.z & 0xffff, xv.z >> 16, xv.w & 0xffff, xv.w >> 16};
+            uint32_t e[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                e[q] = run;
+                run += h[q];
+            }
+            c4[d * V + v] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
         }
-        c4[d] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
     }
-    if (tid == NT - 1) dstart[ndig] = (uint16_t)run;
+    if (tid == T - 1) dstart[ndig] = (uint16_t)run;
     __syncthreads();
 }
 
-template <int KK, int PB>
-__global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                                   const uint32_t *__restrict__ mat, int dst_sel) {
+template <int KK, int PB, int SW>
+__global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
+                                                              int nseg, const uint32_t *__restrict__ mat,
+                                                              int dst_sel, long long *prof) {
+    long long t_mark = prof ? clock64() : 0;
+    long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
+#define SCAT_MARK(slot)                                  \
+    do {                                                 \
+        if (prof) {                                      \
+            long long t_ = clock64();                    \
+            acc_ph[slot] += t_ - t_mark;                 \
+            t_mark = t_;                                 \
+        }                                                \
+    } while (0)
     using P = typename PayloadT<PB>::T;
     constexpr int ITEMS = SCAT_ITEMS;
+    constexpr int ST = SW * 32;             // threads
+    constexpr int ROUND = ST * ITEMS;       // records per round
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t wtot[NWARPS];
+    __shared__ uint32_t wtot[SW];
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
     const int64_t ti = blockIdx.x - p.tile_first;
@@ -604,46 +639,58 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *_
     if (p.mode == MODE_COPY) {  // all-equal segment: land it in the output directly
         if (p.src == 2) return;
         P *op = (P *)B.out_p;
-        for (int64_t i = t0 + threadIdx.x; i < t1; i += NT) {
+        for (int64_t i = t0 + threadIdx.x; i < t1; i += ST) {
             B.out_k[i] = sk[i];
             if constexpr (PB != 0) op[i] = sp[i];
         }
         return;
     }
     const int k = p.k;
-    const ScatLayout L = scat_layout(k, PB);
+    const ScatLayout L = scat_layout(k, PB, SW);
     uint32_t *cur = (uint32_t *)(smem + L.off_cur);
     uint16_t *cnt = (uint16_t *)(smem + L.off_cnt);
     uint16_t *lst = (uint16_t *)(smem + L.off_lst);
     uint64_t *stk = (uint64_t *)(smem + L.off_k);
     P *stp = (P *)(smem + L.off_p);
     uint16_t *stb = (uint16_t *)(smem + L.off_b);
+    double *cdf = (double *)(smem + L.off_cdf);
+    if (p.mode == MODE_ZCDF)
+        for (int q = threadIdx.x; q <= p.kf; q += ST) cdf[q] = B.cdf[q];
     uint64_t *dk = dst_sel == 1 ? B.tmp_k : B.out_k;
     P *dp = (P *)(dst_sel == 1 ? B.tmp_p : B.out_p);
     const uint32_t *col = mat + p.mat_base + ti;
     const uint32_t adj = (uint32_t)(p.start - p.scan_base);
-    const int NC = k * NWARPS;
-    for (int b = threadIdx.x; b < k; b += NT) cur[b] = col[(int64_t)b * p.ntiles] + adj;
-    for (int q = threadIdx.x; q < NC; q += NT) cnt[q] = 0;
+    const int NC = k * SW;
+    for (int b = threadIdx.x; b < k; b += ST) cur[b] = col[(int64_t)b * p.ntiles] + adj;
+    for (int q = threadIdx.x; q < NC; q += ST) cnt[q] = 0;
     __syncthreads();
 
     const int w = threadIdx.x >> 5, lane = lane_id();
     const unsigned lt = lanemask_lt();
-    for (int64_t r0 = t0; r0 < t1; r0 += SCAT_ROUND) {
-        const int nvalid = (int)min((int64_t)SCAT_ROUND, t1 - r0);
-        const int base = w * 32 * ITEMS + lane;
-        uint64_t key[ITEMS];
+    // Software pipeline: the keys of round r+1 are loaded right after round
+    // r's placement (key[] is free then) and land during its write phase;
+    // payload loads are issued at the start of a round and consumed only at
+    // placement, behind the bucket / count / scan phases.
+    const int base = w * 32 * ITEMS + lane;
+    uint64_t key[ITEMS];
+    {
+        const int nv0 = (int)min((int64_t)ROUND, t1 - t0);
+#pragma unroll
+        for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nv0 ? __ldcs(sk + t0 + base + j * 32) : 0ull;
+    }
+    for (int64_t r0 = t0; r0 < t1; r0 += ROUND) {
+        SCAT_MARK(5);
+        const int nvalid = (int)min((int64_t)ROUND, t1 - r0);
         P pay[ITEMS];
         int bk[ITEMS];
+        if constexpr (PB != 0) {
 #pragma unroll
-        for (int j = 0; j < ITEMS; j++) {
-            const int i = base + j * 32;
-            key[j] = i < nvalid ? __ldcs(sk + r0 + i) : 0ull;
-            if constexpr (PB != 0) pay[j] = i < nvalid ? __ldcs(sp + r0 + i) : (P)0;
+            for (int j = 0; j < ITEMS; j++) pay[j] = base + j * 32 < nvalid ? __ldcs(sp + r0 + base + j * 32) : (P)0;
         }
 #pragma unroll
         for (int j = 0; j < ITEMS; j++)
-            bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts) : -1;
+            bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
+        SCAT_MARK(0);  // loads + bucket ids
         // count per (bucket, warp): all MATCH.ANY issued back to back, the
         // leaders add with shared atomics on the containing 32-bit word
         unsigned peers[ITEMS];
@@ -652,20 +699,22 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *_
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
             if (bk[j] >= 0 && (peers[j] & lt) == 0) {
-                const int q = bk[j] * NWARPS + w;
+                const int q = bk[j] * SW + w;
                 atomicAdd((uint32_t *)cnt + (q >> 1), (uint32_t)__popc(peers[j]) << (16 * (q & 1)));
             }
         }
         __syncthreads();
-        scan_dw8(cnt, k, lst, wtot);
+        SCAT_MARK(1);  // match + counting
+        scan_dw<SW>(cnt, k, lst, wtot);
+        SCAT_MARK(2);  // scan
         // place (stable local sort by bucket): items in input order
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
             const int leader = __ffs(peers[j]) - 1;
             uint32_t b0 = 0;
             if (bk[j] >= 0 && lane == leader) {
-                b0 = cnt[bk[j] * NWARPS + w];
-                cnt[bk[j] * NWARPS + w] = (uint16_t)(b0 + __popc(peers[j]));
+                b0 = cnt[bk[j] * SW + w];
+                cnt[bk[j] * SW + w] = (uint16_t)(b0 + __popc(peers[j]));
             }
             __syncwarp();
             b0 = __shfl_sync(0xffffffffu, b0, leader);
@@ -677,17 +726,96 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(Buffers B, const SegParams *_
             }
         }
         __syncthreads();
+        SCAT_MARK(3);  // placement
+        {  // prefetch the next round's keys
+            const int64_t rn = r0 + ROUND;
+            const int nvn = rn < t1 ? (int)min((int64_t)ROUND, t1 - rn) : 0;
+#pragma unroll
+            for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nvn ? __ldcs(sk + rn + base + j * 32) : 0ull;
+        }
         // coalesced run writes, counters reset for the next round
-        for (int i = threadIdx.x; i < nvalid; i += NT) {
+        for (int i = threadIdx.x; i < nvalid; i += ST) {
             const int b = stb[i];
             const uint32_t dst = cur[b] + (uint32_t)(i - lst[b]);
             dk[dst] = stk[i];
             if constexpr (PB != 0) dp[dst] = stp[i];
         }
-        for (int q = threadIdx.x; q < NC; q += NT) cnt[q] = 0;
+        for (int q = threadIdx.x; q < NC; q += ST) cnt[q] = 0;
         __syncthreads();
-        for (int b = threadIdx.x; b < k; b += NT) cur[b] += (uint32_t)(lst[b + 1] - lst[b]);
+        for (int b = threadIdx.x; b < k; b += ST) cur[b] += (uint32_t)(lst[b + 1] - lst[b]);
         __syncthreads();
+        SCAT_MARK(4);  // writes + cursor update
+    }
+    if (prof && threadIdx.x == 0)
+        for (int q = 0; q < 6; q++) prof[(int64_t)blockIdx.x * 8 + q] = acc_ph[q];
+#undef SCAT_MARK
+}
+
+// ------------------------------------------------------- equalisation
+// Level 1, fitted mapping: a histogram of CDF_KNOTS coarse z-score bins (Eq. 1
+// with that many bins) and the piecewise-linear empirical CDF through it, in
+// bucket units; bucket_cdf maps a key through it, so buckets hold ~n/k
+// records whatever the shape of the distribution at the knot resolution.
+// The kernels act only if K1 left the segment in z-score mode.
+
+constexpr int KF_MAX = CDF_KNOTS;
+
+template <int KK>
+__global__ void __launch_bounds__(512) k_fine_hist(const uint64_t *__restrict__ keys, int64_t n,
+                                                   const SegParams *__restrict__ seg, int kf,
+                                                   unsigned int *__restrict__ counts) {
+    extern __shared__ uint32_t fh[];
+    const SegParams p = *seg;
+    if (p.mode != MODE_ZSCORE) return;
+    const double scale_f = p.scale * ((double)kf / (double)p.k);
+    for (int b = threadIdx.x; b < kf; b += 512) fh[b] = 0;
+    __syncthreads();
+    int64_t i = (int64_t)blockIdx.x * 512 + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * 512;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        uint64_t b[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) b[u] = __ldcs(keys + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; u++) atomicAdd(&fh[bucket_z(key_value<KK>(b[u]), p.center, p.std, p.zmin, scale_f, kf)], 1u);
+    }
+    for (; i < n; i += stride) atomicAdd(&fh[bucket_z(key_value<KK>(__ldcs(keys + i)), p.center, p.std, p.zmin, scale_f, kf)], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kf; b += 512)
+        if (fh[b]) atomicAdd(&counts[b], fh[b]);
+}
+
+__global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restrict__ counts, int kf, int64_t n,
+                                                    SegParams *seg, double *cdf) {
+    __shared__ unsigned long long wsum[32];
+    SegParams p = *seg;
+    if (p.mode != MODE_ZSCORE) return;
+    const int per = kf / 1024;  // kf is a multiple of 1024
+    const int f0 = threadIdx.x * per;
+    unsigned long long tsum = 0;
+    for (int q = 0; q < per; q++) tsum += counts[f0 + q];
+    unsigned long long x = tsum;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    unsigned long long run = x - tsum;
+    for (int q = 0; q < w; q++) run += wsum[q];
+    const double inv = (double)p.k / (double)n;  // knots in bucket units
+    for (int q = 0; q < per; q++) {
+        cdf[f0 + q] = (double)run * inv;
+        run += counts[f0 + q];
+    }
+    if (threadIdx.x == 1023) cdf[kf] = (double)p.k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.scale = p.scale * ((double)kf / (double)p.k);
+        p.kf = kf;
+        p.mode = MODE_ZCDF;
+        *seg = p;
     }
 }
 
@@ -720,7 +848,8 @@ __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64
 
 __global__ void k_bstart(const SegParams *__restrict__ segs, int nseg, const int64_t *__restrict__ kfirst,
                          const uint32_t *__restrict__ mat, int64_t *__restrict__ bstart, SegParams *children,
-                         SegAcc *acc, unsigned long long *ctrl, ClassCfg cc, int64_t total_slots) {
+                         SegAcc *acc, unsigned long long *ctrl, ClassCfg cc, int64_t total_slots, Buffers B,
+                         int key_kind) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= total_slots) return;
     const int s = seg_of_slot(kfirst, nseg, g);
@@ -748,6 +877,12 @@ __global__ void k_bstart(const SegParams *__restrict__ segs, int nseg, const int
     if (integer) {
         ch.mode = MODE_INTEGER;
         atomicAdd(&ctrl[C_ST_FALLBACKS], 1ull);
+    } else if (p.mode == MODE_ZCDF) {
+        // an equal-population bucket is not a z-interval: centre the child on
+        // one of its own keys (the first record the scatter placed there)
+        ch.mode = MODE_ZSCORE;
+        const uint64_t kb = src_keys(B, ch.src)[st];
+        ch.center = key_kind ? __longlong_as_double((long long)kb) : __ll2double_rn((long long)kb);
     } else {
         ch.mode = MODE_ZSCORE;
         ch.center = __dadd_rn(__dmul_rn(__dsub_rn(__ddiv_rn((double)b + 0.5, p.scale), p.zmin), p.std), p.center);
@@ -904,15 +1039,15 @@ __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned l
 // output store, so src may alias the output (in-place refinement).
 
 constexpr int FIN_INS = 32;         // sub-buckets up to this size are ranked by comparison
-constexpr int FIN_SBITS_MAX = 12;   // <= 4096 sub-buckets (16-bit cursors)
-constexpr int FIN_BIG_MAX = 256;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
+constexpr int FIN_SBITS_MAX = 13;   // <= 8192 sub-buckets (16-bit cursors)
+constexpr int FIN_BIG_MAX = 512;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
 
 constexpr int FT = 512;         // threads per finish CTA
 constexpr int FW = FT / 32;     // warps per finish CTA
 
 template <int PB>
 struct FinItems {
-    static constexpr int F = PB == 8 ? 8 : (PB == 4 ? 12 : 16);  // records per thread; cap = FT * F
+    static constexpr int F = PB == 8 ? 16 : 24;  // records per thread; cap = FT * F
 };
 
 struct FinLayout {
@@ -945,7 +1080,7 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
 }
 
 template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 2) k_finish(Buffers B, const Entry *__restrict__ entries, int cap,
+__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries, int cap,
                                                   Entry *refine, unsigned long long *refine_count, int fin_ins,
                                                   long long *prof) {
 #define FIN_MARK(slot)                                                                                   \
@@ -966,7 +1101,7 @@ __global__ void __launch_bounds__(FT, 2) k_finish(Buffers B, const Entry *__rest
     uint32_t *bigmask = (uint32_t *)(smem + L.off_bcnt + FIN_BIG_MAX * FW * 2);
     __shared__ unsigned long long r_min[FW], r_max[FW];
     __shared__ uint32_t wsum[FW];
-    __shared__ uint32_t negzero[256];  // float64: bit per record index that was -0.0 (cap <= 8192)
+    __shared__ uint32_t negzero[FT];  // float64: bit per record index that was -0.0 (cap <= 16384)
     __shared__ int nbig;
     __shared__ uint16_t bslot[FIN_BIG_MAX];  // sorted oversized digits
 
@@ -991,7 +1126,7 @@ __global__ void __launch_bounds__(FT, 2) k_finish(Buffers B, const Entry *__rest
     if (tid == 0) nbig = 0;
     bool anyneg = false;
     if constexpr (KK == KEY_F64) {
-        if (tid < 256) negzero[tid] = 0u;
+        negzero[tid] = 0u;
 #pragma unroll
         for (int j = 0; j < F; j++) anyneg |= (o[j] == SIGN);
     }
@@ -1080,7 +1215,7 @@ __global__ void __launch_bounds__(FT, 2) k_finish(Buffers B, const Entry *__rest
     //      multiple of 8 except when S < FT*8); 16-byte vector accesses.
     {
         uint16_t *c16 = (uint16_t *)cw;
-        const int per = S / FT;  // S >= 32; per in {0 (S<FT), 1, 2, 4, 8}
+        const int per = S / FT;  // S >= 32; per in {0 (S<FT), 1, 2, 4, 8, 16}
         const int d0 = per ? tid * per : (tid < S ? tid : S), d1 = per ? d0 + per : (tid < S ? tid + 1 : S);
         uint16_t v[16];
         uint32_t tsum = 0;

@@ -142,10 +142,11 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
     if (cfg.mapping == ZSB_MAP_PAPER) {
         P.k = std::min<int64_t>(cluster_count(n, cfg.alpha), K_LEVEL1_MAX);
     } else {
-        int64_t kmax = env_int("ZSB_K1MAX", 1024);
+        int64_t kmax = env_int("ZSB_K1MAX", 1024);  // runs of >= 4 records per 4096-record round
         P.k = std::min<int64_t>(std::max<int64_t>(16, pow2_at_least((4 * n + P.cap - 1) / P.cap)), kmax);
     }
-    int64_t target_tiles = (int64_t)num_sms() * env_int("ZSB_TILES_PER_SM", 2);
+    int64_t target_tiles =
+        (int64_t)num_sms() * env_int("ZSB_TILES_PER_SM", scat_warps((int)P.k, env_int("ZSB_SW16_ABOVE", 512)) == 8 ? 2 : 1);
     int64_t tl = std::max<int64_t>(4 * P.k, (n + target_tiles - 1) / target_tiles);
     tl = std::max<int64_t>(tl, 2048);
     tl = (tl + 255) & ~(int64_t)255;
@@ -156,7 +157,7 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
 
 struct Layout {
     size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, wfirst, bstart, entries, refine0, refine1, parts,
-        ctrl, dbg, total;
+        ctrl, dbg, fine, lut, total;
     int64_t mat_cap, seg_cap, ent_cap, status_cap, slot_cap, ref_cap;
 };
 
@@ -206,6 +207,10 @@ Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
     o = align_up(o + C_SLOTS * 8);
     L.dbg = o;
     o = align_up(o + 16 * 8);
+    L.fine = o;
+    o = align_up(o + (size_t)KF_MAX * 4);
+    L.lut = o;
+    o = align_up(o + (size_t)(KF_MAX + 1) * 8);
     L.total = o;
     return L;
 }
@@ -260,16 +265,43 @@ struct Ctx {
     int64_t n;
 };
 
+long long *g_scat_prof = nullptr;
+int64_t g_scat_prof_n = 0;
+long long *scat_prof(int64_t n) {
+    if (!env_int("ZSB_FIN_PROFILE", 0) || n < g_scat_prof_n) return nullptr;
+    if (g_scat_prof) cudaFree(g_scat_prof);
+    cudaMalloc(&g_scat_prof, (size_t)n * 8 * 8);
+    cudaMemset(g_scat_prof, 0, (size_t)n * 8 * 8);
+    g_scat_prof_n = n;
+    return g_scat_prof;
+}
+
+void scat_prof_dump() {
+    if (!g_scat_prof) return;
+    std::vector<long long> h((size_t)g_scat_prof_n * 8);
+    cudaMemcpy(h.data(), g_scat_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    double acc[6] = {0};
+    for (int64_t b = 0; b < g_scat_prof_n; b++)
+        for (int q = 0; q < 6; q++) acc[q] += (double)h[(size_t)b * 8 + q];
+    fprintf(stderr, "[zsb] scatter phases per CTA (cycles, summed over rounds): loads+buckets %.0f match+count %.0f "
+                    "scan %.0f place %.0f write %.0f loop %.0f\n", acc[0] / g_scat_prof_n, acc[1] / g_scat_prof_n,
+            acc[2] / g_scat_prof_n, acc[3] / g_scat_prof_n, acc[4] / g_scat_prof_n, acc[5] / g_scat_prof_n);
+    cudaFree(g_scat_prof);
+    g_scat_prof = nullptr;
+    g_scat_prof_n = 0;
+}
+
 template <int KK, int PB>
-int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel) {
+int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
+                     bool segs_level1 = false) {
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
-    size_t kbytes = (size_t)kmax * 4;
+    size_t kbytes = (size_t)((kmax + 1) & ~1) * 4 + (size_t)(CDF_KNOTS + 1) * 8;
     smem_optin(k_hist<KK>, kbytes);
     {
         PhaseScope ph(PH_HIST, c.st);
-        k_hist<KK><<<(unsigned)tiles, NT, kbytes, c.st>>>(c.B, segs, nseg, mat);
+        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat);
     }
     ZSB_LAUNCH("k_hist");
     int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
@@ -280,11 +312,17 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
         k_scan<<<(unsigned)sblocks, NT, 0, c.st>>>(mat, mat_entries, status, ctrl);
     }
     ZSB_LAUNCH("k_scan");
-    const size_t sbytes = scat_layout(kmax, PB).total;
-    smem_optin(k_scatter<KK, PB>, sbytes);
-    {
+    const size_t cdf_bytes = (c.B.cdf && segs_level1) ? (size_t)(CDF_KNOTS + 1) * 8 : 0;
+    if (scat_warps(kmax, env_int("ZSB_SW16_ABOVE", 512)) == 8) {
+        const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
+        smem_optin(k_scatter<KK, PB, 8>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB><<<(unsigned)tiles, NT, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel);
+        k_scatter<KK, PB, 8><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
+    } else {
+        const size_t sbytes = scat_layout(kmax, PB, 16).total + cdf_bytes;
+        smem_optin(k_scatter<KK, PB, 16>, sbytes);
+        PhaseScope ph(PH_SCATTER, c.st);
+        k_scatter<KK, PB, 16><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
@@ -410,6 +448,17 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                                              nullptr);
     }
     ZSB_LAUNCH("k_moments");
+    if (cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0)) {
+        // histogram equalisation of level 1 (acts only if K1 chose z-score mode)
+        unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
+        ZSB_CUDA(cudaMemsetAsync(fine, 0, (size_t)KF_MAX * 4, c.st));
+        {
+            PhaseScope ph(PH_MOMENTS, c.st, 2);
+            k_fine_hist<KK><<<num_sms() * 2, 512, (size_t)KF_MAX * 4, c.st>>>(c.B.in_k, n, seg_cur, KF_MAX, fine);
+            k_build_cdf<<<1, 1024, 0, c.st>>>(fine, KF_MAX, n, seg_cur, (double *)(c.ws + c.L.lut));
+        }
+        ZSB_LAUNCH("k_fine_hist/k_build_cdf");
+    }
 
     int nseg = 1;
     int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
@@ -426,13 +475,14 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             ZSB_LAUNCH("k_seg_moments/params");
         }
         const int dst_sel = (level == 1) ? 1 : ((level % 2 == 0) ? 2 : 1);
-        int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel);
+        int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel, level == 1);
         if (rc) return rc;
         ZSB_CUDA(cudaMemsetAsync(ctrl + C_NCHILD, 0, 16, c.st));  // C_NCHILD, C_NENTRY
         {
             PhaseScope ph(PH_CLASSIFY, c.st, 3);
             k_bstart<<<(unsigned)((total_slots + 255) / 256), 256, 0, c.st>>>(seg_cur, nseg, kfirst, mat, bstart,
-                                                                             seg_next, acc, ctrl, cc, total_slots);
+                                                                             seg_next, acc, ctrl, cc, total_slots,
+                                                                             c.B, KK);
             k_windows<<<(unsigned)((total_windows + 255) / 256), 256, 0, c.st>>>(seg_cur, nseg, kfirst, wfirst, bstart,
                                                                                entries, ctrl, cc, total_windows);
             k_plan<<<1, 1024, 0, c.st>>>(seg_next, ctrl + C_NCHILD, kfirst, wfirst, ctrl, (int32_t)c.P.cap,
@@ -482,7 +532,10 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     timing_collect();
     int rc3 = drain_refine((int64_t)h_ctrl[r ? C_NREF1 : C_NREF0]);
     if (rc3) return rc3;
-    if (env_int("ZSB_FIN_PROFILE", 0)) fin_prof_dump();
+    if (env_int("ZSB_FIN_PROFILE", 0)) {
+        fin_prof_dump();
+        scat_prof_dump();
+    }
     stats[ZSB_STAT_MAX_DEPTH] = (int64_t)h_ctrl[C_ST_MAXDEPTH];
     stats[ZSB_STAT_FALLBACKS] = (int64_t)h_ctrl[C_ST_FALLBACKS];
     stats[ZSB_STAT_SCATTERS] = (int64_t)h_ctrl[C_ST_SCATTERS];
@@ -590,6 +643,7 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     ctx.B.out_k = (uint64_t *)d_out_keys;
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = nullptr;
+    ctx.B.cdf = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0],
@@ -703,6 +757,7 @@ int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32
     ctx.B.out_k = (uint64_t *)d_out_keys;
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = nullptr;
+    ctx.B.cdf = (const double *)(ctx.ws + ctx.L.lut);
     return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats);
 }
 
@@ -752,10 +807,10 @@ int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double
     size_t kb = (size_t)k * 4;
     if (key_dtype == ZSB_KEY_I64) {
         smem_optin(k_hist<0>, kb);
-        k_hist<0><<<(unsigned)ctx.P.ntiles, NT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
+        k_hist<0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
     } else {
         smem_optin(k_hist<1>, kb);
-        k_hist<1><<<(unsigned)ctx.P.ntiles, NT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
+        k_hist<1><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
     }
     ZSB_LAUNCH("k_hist");
     k_bucket_totals<<<(unsigned)((k + 255) / 256), 256, 0, ctx.st>>>(mat, k, ctx.P.ntiles, d_counts);
@@ -950,6 +1005,7 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ctx.B.out_k = (uint64_t *)d_out_keys;
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = dc;
+    ctx.B.cdf = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, nparts, ctx.P.tile_len, ctx.P.ntiles, 0, 0.0, 1.0,
