@@ -101,7 +101,9 @@ enum Ctrl {
     C_WIN_NEXT = 13,
     C_NREF0 = 14,
     C_NREF1 = 15,
-    C_SLOTS = 16
+    C_FTICK0 = 16,  // finish work tickets (dynamic scheduling), one per launch in a pair
+    C_FTICK1 = 17,
+    C_SLOTS = 24
 };
 
 // ------------------------------------------------------------ key traits

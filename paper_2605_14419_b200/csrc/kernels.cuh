@@ -609,6 +609,44 @@ __device__ __forceinline__ void scan_dw(uint16_t *cnt, int ndig, uint16_t *dstar
     __syncthreads();
 }
 
+// Exclusive scan in (digit, warp) order of per-(warp, digit) u16 counters laid
+// out [warp][ndig] (a warp's leaders then touch distinct banks).  Thread t
+// owns digits [t*per, (t+1)*per): per digit it walks the SW warps in order,
+// then one block scan of the thread totals and a write-back pass.  Writes the
+// digit starts to dstart[0..ndig].  Ends with a barrier.
+template <int SW>
+__device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstart, uint32_t *wsum) {
+    constexpr int T = SW * 32;
+    const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+    const int per = (ndig + T - 1) / T;
+    const int d0 = min(ndig, tid * per), d1 = min(ndig, d0 + per);
+    uint32_t tsum = 0;
+    for (int d = d0; d < d1; d++)
+#pragma unroll
+        for (int ww = 0; ww < SW; ww++) tsum += cnt[ww * ndig + d];
+    uint32_t x = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    uint32_t run = x - tsum;
+    for (int q = 0; q < w; q++) run += wsum[q];
+    for (int d = d0; d < d1; d++) {
+        dstart[d] = (uint16_t)run;
+#pragma unroll
+        for (int ww = 0; ww < SW; ww++) {
+            const uint32_t c = cnt[ww * ndig + d];
+            cnt[ww * ndig + d] = (uint16_t)run;
+            run += c;
+        }
+    }
+    if (tid == T - 1) dstart[ndig] = (uint16_t)run;
+    __syncthreads();
+}
+
 template <int KK, int PB, int SW>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
@@ -699,13 +737,13 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
             if (bk[j] >= 0 && (peers[j] & lt) == 0) {
-                const int q = bk[j] * SW + w;
+                const int q = w * k + bk[j];
                 atomicAdd((uint32_t *)cnt + (q >> 1), (uint32_t)__popc(peers[j]) << (16 * (q & 1)));
             }
         }
         __syncthreads();
         SCAT_MARK(1);  // match + counting
-        scan_dw<SW>(cnt, k, lst, wtot);
+        scan_wd<SW>(cnt, k, lst, wtot);
         SCAT_MARK(2);  // scan
         // place (stable local sort by bucket): items in input order
 #pragma unroll
@@ -713,8 +751,8 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
             const int leader = __ffs(peers[j]) - 1;
             uint32_t b0 = 0;
             if (bk[j] >= 0 && lane == leader) {
-                b0 = cnt[bk[j] * SW + w];
-                cnt[bk[j] * SW + w] = (uint16_t)(b0 + __popc(peers[j]));
+                b0 = cnt[w * k + bk[j]];
+                cnt[w * k + bk[j]] = (uint16_t)(b0 + __popc(peers[j]));
             }
             __syncwarp();
             b0 = __shfl_sync(0xffffffffu, b0, leader);
@@ -1080,12 +1118,11 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
 }
 
 template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries, int cap,
-                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
-                                                  long long *prof) {
+__device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, int64_t eidx, int cap, Entry *refine,
+                                             unsigned long long *refine_count, int fin_ins, long long *prof) {
 #define FIN_MARK(slot)                                                                                   \
     do {                                                                                                 \
-        if (prof && threadIdx.x == 0) prof[(int64_t)blockIdx.x * 8 + (slot)] = clock64();              \
+        if (prof && threadIdx.x == 0) prof[eidx * 8 + (slot)] = clock64();                              \
     } while (0)
     FIN_MARK(0);
     using P = typename PayloadT<PB>::T;
@@ -1105,7 +1142,6 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
     __shared__ int nbig;
     __shared__ uint16_t bslot[FIN_BIG_MAX];  // sorted oversized digits
 
-    const Entry e = entries[blockIdx.x];
     const int m = e.len;
     if (m <= 0) return;
     const uint64_t *sk = src_keys(B, e.src) + e.start;
@@ -1400,6 +1436,30 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
     FIN_MARK(5);
     FIN_MARK(6);
 #undef FIN_MARK
+}
+
+// Persistent finish: the work count is read from device memory (written by
+// the classify or a previous finish), so the host enqueues without a sync.
+template <int KK, int PB>
+__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
+                                                  const unsigned long long *count, int64_t count_const, int cap,
+                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
+                                                  long long *prof, unsigned long long *ticket) {
+    __shared__ long long next;
+    const int64_t ne = count ? (int64_t)*count : count_const;
+    if (!ticket) {  // one run per CTA (grid = exact count)
+        if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
+                                                           fin_ins, prof);
+        return;
+    }
+    while (true) {  // dynamic scheduling: a CTA takes the next run as soon as it is free
+        if (threadIdx.x == 0) next = (long long)atomicAdd(ticket, 1ull);
+        __syncthreads();
+        const int64_t i = next;
+        if (i >= ne) break;
+        finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof);
+        __syncthreads();
+    }
 }
 
 // Entry builder for the small-n path (one finish over the whole input).

@@ -361,18 +361,25 @@ void fin_prof_dump() {
     g_fin_prof_n = 0;
 }
 
+// Persistent finish over `list`: count from device memory (count_dev) or a
+// host constant; records refine runs into list `ref_out` (0/1).
 template <int KK, int PB>
-int launch_finish(Ctx &c, const Entry *list, int64_t nentries, int ref_out) {
-    if (nentries <= 0) return ZSB_OK;
+int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev, int64_t count_const,
+                  int64_t count_bound, int ref_out, int tick) {
+    if (count_bound <= 0) return ZSB_OK;
     FinLayout FL = fin_layout((int)c.P.cap, PB);
     smem_optin(k_finish<KK, PB>, FL.total);
     Entry *refine = (Entry *)(c.ws + (ref_out ? c.L.refine1 : c.L.refine0));
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+    // exact host-known count: one run per CTA; device-side count: persistent CTAs
+    const int64_t grid = count_dev ? std::min<int64_t>(count_bound, (int64_t)num_sms()) : count_bound;
     {
         PhaseScope ph(PH_FINISH, c.st);
-        k_finish<KK, PB><<<(unsigned)nentries, FT, FL.total, c.st>>>(c.B, list, (int)c.P.cap, refine,
-                                                                     ctrl + (ref_out ? C_NREF1 : C_NREF0),
-                                                                     env_int("ZSB_FIN_INS", FIN_INS), fin_prof(nentries));
+        k_finish<KK, PB><<<(unsigned)grid, FT, FL.total, c.st>>>(c.B, list, count_dev, count_const, (int)c.P.cap, refine,
+                                                                ctrl + (ref_out ? C_NREF1 : C_NREF0),
+                                                                env_int("ZSB_FIN_INS", FIN_INS),
+                                                                fin_prof(count_bound),
+                                                                count_dev ? ctrl + C_FTICK0 + tick : nullptr);
     }
     ZSB_LAUNCH("k_finish");
     return ZSB_OK;
@@ -394,22 +401,32 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int64_t stats[ZSB_STAT_SLOTS] = {0, 0, 0, 0, 0};
     unsigned long long h_ctrl[C_SLOTS];
     ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
-    int r = 0;  // refine list the finish launches of this round append to
 
-    // Drain refinement runs (oversized unsorted sub-buckets re-finished in place).
+    // Finish the runs listed in `list` (count on device) and their refine
+    // runs once, without a host round trip; returns after enqueueing.
+    // Refine runs of the refine pass land in list 1 (count C_NREF1).
+    auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
+                              int64_t bound) -> int {
+        ZSB_CUDA(cudaMemsetAsync(ctrl + C_NREF0, 0, 32, c.st));  // C_NREF0, C_NREF1, C_FTICK0, C_FTICK1
+        int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 0, 0);
+        if (rc) return rc;
+        return launch_finish<KK, PB>(c, refine[0], ctrl + C_NREF0, 0, std::min<int64_t>(bound, c.L.ref_cap), 1, 1);
+    };
+    // After a sync: drain refine runs of refine runs (rare), ping-ponging lists.
     auto drain_refine = [&](int64_t pending) -> int {
+        int src = 1;
         while (pending > 0) {
             if (pending > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-            int rc0 = cudaMemsetAsync(ctrl + (r ? C_NREF0 : C_NREF1), 0, 8, c.st) == cudaSuccess ? 0 : 1;
-            if (rc0) return fail(ZSB_ERR_CUDA, "memset");
-            int rc = launch_finish<KK, PB>(c, refine[r], pending, 1 - r);
+            ZSB_CUDA(cudaMemsetAsync(ctrl + (src ? C_NREF0 : C_NREF1), 0, 8, c.st));
+            ZSB_CUDA(cudaMemsetAsync(ctrl + C_FTICK0, 0, 8, c.st));
+            int rc = launch_finish<KK, PB>(c, refine[src], nullptr, pending, pending, 1 - src, 0);
             if (rc) return rc;
             stats[ZSB_STAT_INSERTION] += pending;
-            r = 1 - r;
             ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
             ZSB_CUDA(cudaStreamSynchronize(c.st));
             timing_collect();
-            pending = (int64_t)h_ctrl[r ? C_NREF1 : C_NREF0];
+            src = 1 - src;
+            pending = (int64_t)h_ctrl[src ? C_NREF1 : C_NREF0];
         }
         return ZSB_OK;
     };
@@ -420,13 +437,13 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             k_single_entry<<<1, 1, 0, c.st>>>(entries, n);
         }
         ZSB_LAUNCH("k_single_entry");
-        int rc = launch_finish<KK, PB>(c, entries, 1, r);
+        int rc = enqueue_finish(entries, nullptr, 1, 1);
         if (rc) return rc;
         ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
         ZSB_CUDA(cudaStreamSynchronize(c.st));
         timing_collect();
-        stats[ZSB_STAT_INSERTION] = 1;
-        rc = drain_refine((int64_t)h_ctrl[r ? C_NREF1 : C_NREF0]);
+        stats[ZSB_STAT_INSERTION] = 1 + (int64_t)h_ctrl[C_NREF0];
+        rc = drain_refine((int64_t)h_ctrl[C_NREF1]);
         if (rc) return rc;
         if (h_stats) memcpy(h_stats, stats, sizeof(stats));
         return ZSB_OK;
@@ -464,7 +481,6 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
     int kmax = (int)c.P.k;
     int level = 1;
-    int64_t pending_refine = 0;
     while (true) {
         if (level > 1) {
             {
@@ -489,31 +505,38 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                                          (int32_t)c.P.half, KMAX_CHILD, MIN_TILE);
         }
         ZSB_LAUNCH("k_bstart/k_windows/k_plan");
-        if (env_int("ZSB_DEBUG", 0) >= 2) {  // validate this level's partition on the host
-            ZSB_CUDA(cudaStreamSynchronize(c.st));
-        }
         ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
         ZSB_CUDA(cudaStreamSynchronize(c.st));
         timing_collect();
         if (h_ctrl[C_STATUS] == 3) return fail(ZSB_ERR_NAN, "NaN keys have no order");
+        const int64_t nentry = (int64_t)h_ctrl[C_NENTRY];
+        if (nentry > c.L.ent_cap) return fail(ZSB_ERR_WORKSPACE, "finish list overflow");
+        if (level > 1) {  // refine runs of the previous level's finish, and of their refinement
+            if ((int64_t)h_ctrl[C_NREF0] > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
+            stats[ZSB_STAT_INSERTION] += (int64_t)h_ctrl[C_NREF0];
+            rc = drain_refine((int64_t)h_ctrl[C_NREF1]);
+            if (rc) return rc;
+        }
+        // this level's finish runs (one per CTA) and their refine runs (persistent,
+        // count on device), enqueued back to back; the next level starts right after
+        rc = enqueue_finish(entries, nullptr, nentry, nentry);
+        if (rc) return rc;
         if (env_int("ZSB_DEBUG", 0))
-            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %llu entries %llu refine %llu "
-                            "fallbacks %llu\n", level, nseg, (long long)tiles, kmax, h_ctrl[C_NCHILD],
-                    h_ctrl[C_NENTRY], h_ctrl[r ? C_NREF1 : C_NREF0], h_ctrl[C_ST_FALLBACKS]);
-        // finish runs of this level, plus refinement runs produced before this sync
-        pending_refine = (int64_t)h_ctrl[r ? C_NREF1 : C_NREF0];
-        int64_t nentry = (int64_t)h_ctrl[C_NENTRY];
-        if (nentry > c.L.ent_cap) return fail(ZSB_ERR_WORKSPACE, "finish entry list overflow");
-        if (pending_refine > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-        ZSB_CUDA(cudaMemsetAsync(ctrl + (r ? C_NREF0 : C_NREF1), 0, 8, c.st));
-        int rc2 = launch_finish<KK, PB>(c, entries, nentry, 1 - r);
-        if (rc2) return rc2;
-        rc2 = launch_finish<KK, PB>(c, refine[r], pending_refine, 1 - r);
-        if (rc2) return rc2;
-        stats[ZSB_STAT_INSERTION] += nentry + pending_refine;
-        r = 1 - r;
+            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %llu entries %lld fallbacks %llu\n",
+                    level, nseg, (long long)tiles, kmax, h_ctrl[C_NCHILD], (long long)nentry,
+                    h_ctrl[C_ST_FALLBACKS]);
+        stats[ZSB_STAT_INSERTION] += nentry;
         int64_t nchild = (int64_t)h_ctrl[C_NCHILD];
-        if (nchild == 0) break;
+        if (nchild == 0) {
+            ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
+            ZSB_CUDA(cudaStreamSynchronize(c.st));
+            timing_collect();
+            if ((int64_t)h_ctrl[C_NREF0] > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
+            stats[ZSB_STAT_INSERTION] += (int64_t)h_ctrl[C_NREF0];
+            rc = drain_refine((int64_t)h_ctrl[C_NREF1]);
+            if (rc) return rc;
+            break;
+        }
         if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
         nseg = (int)nchild;
         tiles = (int64_t)h_ctrl[C_TILES_NEXT];
@@ -527,11 +550,6 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         level++;
         if (level > 200) return fail(ZSB_ERR_CUDA, "partition did not terminate");
     }
-    ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
-    ZSB_CUDA(cudaStreamSynchronize(c.st));
-    timing_collect();
-    int rc3 = drain_refine((int64_t)h_ctrl[r ? C_NREF1 : C_NREF0]);
-    if (rc3) return rc3;
     if (env_int("ZSB_FIN_PROFILE", 0)) {
         fin_prof_dump();
         scat_prof_dump();
