@@ -44,7 +44,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-o", LIB + ".tmp", *SOURCES]
+    extra = ["-DZSB_PHASE_PROFILE"] if os.environ.get("ZSB_PHASE_PROFILE") == "1" else []
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", LIB + ".tmp", *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

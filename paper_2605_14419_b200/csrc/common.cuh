@@ -65,6 +65,7 @@ struct SegParams {
     int32_t src;       // buffer holding the segment: 0 = input, 1 = tmp, 2 = out
     int32_t kf;        // MODE_ZCDF: coarse z-bins of the CDF table (scale is the coarse scale)
     int32_t pad;
+    float za, zb;      // MODE_ZCDF: coarse coordinate = fmaf((float)(x - center), za, zb)
 };
 
 // Per-segment accumulator for the recursion moments pass (fused_stats_pass,
@@ -162,37 +163,59 @@ __device__ __forceinline__ int32_t dest_of(uint64_t bits, int64_t pos, const Des
     return d;
 }
 
-// Histogram-equalised z-score bucket: h = Eq. 1 coordinate over kf coarse
-// z-bins (unfloored); within coarse bin s the bucket interpolates the
-// empirical CDF linearly, cdf[s] .. cdf[s+1] (cdf in bucket units, cdf[0] = 0,
-// cdf[kf] = k).  Clamping each bin to [floor(cdf[s]), floor(cdf[s+1])] keeps
-// the map monotone in the key under any rounding.
-__device__ __forceinline__ int32_t bucket_cdf(double x, const SegParams &p, const double *cdf) {
-    const double h = __dmul_rn(__dadd_rn(__ddiv_rn(__dsub_rn(x, p.center), p.std), p.zmin), p.scale);
-    double fs = floor(h);
+// Coefficients of the level-1 coarse coordinate h = ((x - center)/std + zmin)
+// * scale_f, evaluated as fmaf((float)(x - center), za, zb): one fp64
+// subtraction, a conversion and one fp32 FMA.  Every step is a rounded
+// monotone map (za > 0), so h is non-decreasing in the key, which is all the
+// equalised partition needs (the final order never depends on bucket ids,
+// only on their monotonicity).  Returns false if the pair is unusable
+// (degenerate std), in which case the level keeps the exact Eq. 1 mapping.
+__device__ __forceinline__ bool zc_coeffs(const SegParams &p, int kf, float &za, float &zb) {
+    const double sf = p.scale * ((double)kf / (double)p.k);
+    za = (float)(sf / p.std);
+    zb = (float)(p.zmin * sf);
+    return za > 0.0f && za < 3.0e38f && fabsf(zb) < 3.0e38f;
+}
+
+__device__ __forceinline__ float zc_coord(double x, double center, float za, float zb) {
+    return fmaf((float)__dsub_rn(x, center), za, zb);
+}
+
+__device__ __forceinline__ int zc_bin(float h, int kf) {
+    const float f = floorf(h);
+    return !(f > 0.0f) ? 0 : (f >= (float)kf ? kf - 1 : (int)f);
+}
+
+// Histogram-equalised bucket: within coarse bin s the bucket interpolates the
+// empirical CDF linearly between knots kn[s] = (cdf[s], cdf[s+1]) (bucket
+// units, cdf[0] = 0, cdf[kf] = k).  Clamping each bin to [floor(cdf[s]),
+// floor(cdf[s+1])] keeps the map monotone in the key under any rounding.
+__device__ __forceinline__ int32_t bucket_cdf(double x, const SegParams &p, const float2 *kn) {
+    const float h = zc_coord(x, p.center, p.za, p.zb);
+    const float fs = floorf(h);
     int s;
-    double fr;
-    if (!(fs > 0.0)) {
+    float fr;
+    if (!(fs > 0.0f)) {
         s = 0;
-        fr = h > 0.0 ? h : 0.0;
-    } else if (fs >= (double)p.kf) {
+        fr = h > 0.0f ? h : 0.0f;
+    } else if (fs >= (float)p.kf) {
         s = p.kf - 1;
-        fr = 1.0;
+        fr = 1.0f;
     } else {
         s = (int)fs;
         fr = h - fs;
     }
-    const double a = cdf[s], z = cdf[s + 1];
-    const double lo = floor(a), hi = floor(z);
-    double b = floor(__dadd_rn(a, __dmul_rn(fr, __dsub_rn(z, a))));
-    b = b < lo ? lo : (b > hi ? hi : b);
+    const float2 az = kn[s];
+    const float lo = floorf(az.x), hi = floorf(az.y);
+    float b = floorf(fmaf(fr, az.y - az.x, az.x));
+    b = fminf(fmaxf(b, lo), hi);
     const int bi = (int)b;
     return bi < p.k ? bi : p.k - 1;
 }
 
 template <int KK>
 __device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p, int64_t pos = 0,
-                                              const DestCuts *cuts = nullptr, const double *cdf = nullptr) {
+                                              const DestCuts *cuts = nullptr, const float2 *cdf = nullptr) {
     if (p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
     if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
     if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
@@ -241,6 +264,45 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 __device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ------------------------------------------------ TMA bulk copy + mbarrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Order earlier generic-proxy shared-memory accesses before async-proxy (TMA) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// One TMA bulk copy global -> shared (16-byte aligned addresses, size a multiple of 16).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 template <int PB>

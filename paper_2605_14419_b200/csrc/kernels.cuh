@@ -30,7 +30,7 @@ struct Buffers {
     uint64_t *out_k;
     void *out_p;
     const DestCuts *cuts;  // MODE_DEST only
-    const double *cdf;     // MODE_ZCDF only: kf + 1 CDF knots in bucket units (global; staged in smem)
+    const float2 *cdf;     // MODE_ZCDF only: kf knot pairs (cdf[s], cdf[s+1]) in bucket units (staged in smem)
 };
 
 __device__ __forceinline__ const uint64_t *src_keys(const Buffers &B, int src) {
@@ -398,9 +398,9 @@ __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restr
         return;
     }
     for (int b = threadIdx.x; b < p.k; b += HT) hist[b] = 0;
-    double *cdf = (double *)(hist + ((p.k + 1) & ~1));
+    float2 *cdf = (float2 *)(hist + ((p.k + 1) & ~1));
     if (p.mode == MODE_ZCDF)
-        for (int q = threadIdx.x; q <= p.kf; q += HT) cdf[q] = B.cdf[q];
+        for (int q = threadIdx.x; q < p.kf; q += HT) cdf[q] = B.cdf[q];
     __syncthreads();
     const uint64_t *src = src_keys(B, p.src);
     int64_t i = t0 + threadIdx.x;
@@ -651,6 +651,7 @@ template <int KK, int PB, int SW>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
                                                               int dst_sel, long long *prof) {
+#ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
     long long t_mark = prof ? clock64() : 0;
     long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
 #define SCAT_MARK(slot)                                  \
@@ -661,6 +662,11 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
             t_mark = t_;                                 \
         }                                                \
     } while (0)
+#else
+#define SCAT_MARK(slot) \
+    do {                \
+    } while (0)
+#endif
     using P = typename PayloadT<PB>::T;
     constexpr int ITEMS = SCAT_ITEMS;
     constexpr int ST = SW * 32;             // threads
@@ -691,9 +697,9 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     uint64_t *stk = (uint64_t *)(smem + L.off_k);
     P *stp = (P *)(smem + L.off_p);
     uint16_t *stb = (uint16_t *)(smem + L.off_b);
-    double *cdf = (double *)(smem + L.off_cdf);
+    float2 *cdf = (float2 *)(smem + L.off_cdf);
     if (p.mode == MODE_ZCDF)
-        for (int q = threadIdx.x; q <= p.kf; q += ST) cdf[q] = B.cdf[q];
+        for (int q = threadIdx.x; q < p.kf; q += ST) cdf[q] = B.cdf[q];
     uint64_t *dk = dst_sel == 1 ? B.tmp_k : B.out_k;
     P *dp = (P *)(dst_sel == 1 ? B.tmp_p : B.out_p);
     const uint32_t *col = mat + p.mat_base + ti;
@@ -729,16 +735,24 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         for (int j = 0; j < ITEMS; j++)
             bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
         SCAT_MARK(0);  // loads + bucket ids
-        // count per (bucket, warp): all MATCH.ANY issued back to back, the
-        // leaders add with shared atomics on the containing 32-bit word
-        unsigned peers[ITEMS];
-#pragma unroll
-        for (int j = 0; j < ITEMS; j++) peers[j] = __match_any_sync(0xffffffffu, bk[j]);
+        // count per (warp, bucket): all MATCH.ANY issued back to back, the
+        // leaders add with shared atomics on the containing 32-bit word.  What
+        // placement needs of an item is packed into one word (bucket 11 bits,
+        // leader lane 5, rank among its warp peers 5, peer count 6) so the
+        // round keeps one register per item besides its key and payload.
+        uint32_t pk[ITEMS];
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            if (bk[j] >= 0 && (peers[j] & lt) == 0) {
-                const int q = w * k + bk[j];
-                atomicAdd((uint32_t *)cnt + (q >> 1), (uint32_t)__popc(peers[j]) << (16 * (q & 1)));
+            const unsigned m = __match_any_sync(0xffffffffu, bk[j]);
+            pk[j] = bk[j] < 0 ? 0xffffffffu
+                              : (uint32_t)bk[j] | ((uint32_t)(__ffs(m) - 1) << 11) | ((uint32_t)__popc(m & lt) << 16) |
+                                    ((uint32_t)__popc(m) << 21);
+        }
+#pragma unroll
+        for (int j = 0; j < ITEMS; j++) {
+            if (pk[j] != 0xffffffffu && ((pk[j] >> 16) & 31) == 0) {
+                const int q = w * k + (int)(pk[j] & 2047);
+                atomicAdd((uint32_t *)cnt + (q >> 1), (pk[j] >> 21) << (16 * (q & 1)));
             }
         }
         __syncthreads();
@@ -748,19 +762,21 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         // place (stable local sort by bucket): items in input order
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const int leader = __ffs(peers[j]) - 1;
+            const bool valid = pk[j] != 0xffffffffu;
+            const int leader = valid ? (int)((pk[j] >> 11) & 31) : lane;
+            const int b = (int)(pk[j] & 2047);
             uint32_t b0 = 0;
-            if (bk[j] >= 0 && lane == leader) {
-                b0 = cnt[w * k + bk[j]];
-                cnt[w * k + bk[j]] = (uint16_t)(b0 + __popc(peers[j]));
+            if (valid && lane == leader) {
+                b0 = cnt[w * k + b];
+                cnt[w * k + b] = (uint16_t)(b0 + (pk[j] >> 21));
             }
             __syncwarp();
             b0 = __shfl_sync(0xffffffffu, b0, leader);
-            if (bk[j] >= 0) {
-                const uint32_t pos = b0 + __popc(peers[j] & lt);
+            if (valid) {
+                const uint32_t pos = b0 + ((pk[j] >> 16) & 31);
                 stk[pos] = key[j];
                 if constexpr (PB != 0) stp[pos] = pay[j];
-                stb[pos] = (uint16_t)bk[j];
+                stb[pos] = (uint16_t)b;
             }
         }
         __syncthreads();
@@ -784,8 +800,10 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         __syncthreads();
         SCAT_MARK(4);  // writes + cursor update
     }
+#ifdef ZSB_PHASE_PROFILE
     if (prof && threadIdx.x == 0)
         for (int q = 0; q < 6; q++) prof[(int64_t)blockIdx.x * 8 + q] = acc_ph[q];
+#endif
 #undef SCAT_MARK
 }
 
@@ -804,8 +822,9 @@ __global__ void __launch_bounds__(512) k_fine_hist(const uint64_t *__restrict__ 
                                                    unsigned int *__restrict__ counts) {
     extern __shared__ uint32_t fh[];
     const SegParams p = *seg;
-    if (p.mode != MODE_ZSCORE) return;
-    const double scale_f = p.scale * ((double)kf / (double)p.k);
+    float za, zb;
+    if (p.mode != MODE_ZSCORE || !zc_coeffs(p, kf, za, zb)) return;
+    const double c = p.center;
     for (int b = threadIdx.x; b < kf; b += 512) fh[b] = 0;
     __syncthreads();
     int64_t i = (int64_t)blockIdx.x * 512 + threadIdx.x;
@@ -815,19 +834,24 @@ __global__ void __launch_bounds__(512) k_fine_hist(const uint64_t *__restrict__ 
 #pragma unroll
         for (int u = 0; u < 4; u++) b[u] = __ldcs(keys + i + u * stride);
 #pragma unroll
-        for (int u = 0; u < 4; u++) atomicAdd(&fh[bucket_z(key_value<KK>(b[u]), p.center, p.std, p.zmin, scale_f, kf)], 1u);
+        for (int u = 0; u < 4; u++) atomicAdd(&fh[zc_bin(zc_coord(key_value<KK>(b[u]), c, za, zb), kf)], 1u);
     }
-    for (; i < n; i += stride) atomicAdd(&fh[bucket_z(key_value<KK>(__ldcs(keys + i)), p.center, p.std, p.zmin, scale_f, kf)], 1u);
+    for (; i < n; i += stride) atomicAdd(&fh[zc_bin(zc_coord(key_value<KK>(__ldcs(keys + i)), c, za, zb), kf)], 1u);
     __syncthreads();
     for (int b = threadIdx.x; b < kf; b += 512)
         if (fh[b]) atomicAdd(&counts[b], fh[b]);
 }
 
+// Knot pairs (cdf[s], cdf[s+1]) of the piecewise-linear CDF in bucket units
+// (fp32: rounding is monotone, so the knots stay non-decreasing) and the
+// switch of the level-1 segment to MODE_ZCDF.
 __global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restrict__ counts, int kf, int64_t n,
-                                                    SegParams *seg, double *cdf) {
+                                                    SegParams *seg, float2 *cdf) {
     __shared__ unsigned long long wsum[32];
+    __shared__ float knot[KF_MAX + 1];
     SegParams p = *seg;
-    if (p.mode != MODE_ZSCORE) return;
+    float za, zb;
+    if (p.mode != MODE_ZSCORE || !zc_coeffs(p, kf, za, zb)) return;
     const int per = kf / 1024;  // kf is a multiple of 1024
     const int f0 = threadIdx.x * per;
     unsigned long long tsum = 0;
@@ -844,14 +868,17 @@ __global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restri
     for (int q = 0; q < w; q++) run += wsum[q];
     const double inv = (double)p.k / (double)n;  // knots in bucket units
     for (int q = 0; q < per; q++) {
-        cdf[f0 + q] = (double)run * inv;
+        knot[f0 + q] = (float)((double)run * inv);
         run += counts[f0 + q];
     }
-    if (threadIdx.x == 1023) cdf[kf] = (double)p.k;
+    if (threadIdx.x == 1023) knot[kf] = (float)p.k;
     __syncthreads();
+    for (int s = threadIdx.x; s < kf; s += 1024) cdf[s] = make_float2(knot[s], knot[s + 1]);
     if (threadIdx.x == 0) {
         p.scale = p.scale * ((double)kf / (double)p.k);
         p.kf = kf;
+        p.za = za;
+        p.zb = zb;
         p.mode = MODE_ZCDF;
         *seg = p;
     }
@@ -1099,8 +1126,8 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     size_t o = 0;
     L.off_o = o;
     o += (size_t)cap * 8;
-    L.off_pb = o;
-    o += (size_t)cap * pb;
+    L.off_pb = o;  // payload staged in input order by a TMA bulk copy (+16 B alignment slack)
+    o += (size_t)cap * pb + (pb ? 16 : 0);
     o = (o + 15) & ~(size_t)15;
     L.off_i = o;
     o += (size_t)cap * 2;
@@ -1117,9 +1144,36 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     return L;
 }
 
+// Stage src[0, m) into shared memory with the same address phase modulo 16,
+// so element i lands at the returned pointer + i: thread 0 issues one TMA
+// bulk copy of the 16-byte-aligned interior (tracked by `bar`), threads 1..
+// load the ragged head and tail.  Readers wait on `bar` and need a barrier
+// after this call for the plain part.
+template <typename T>
+__device__ __forceinline__ const T *stage_range(unsigned char *area, const T *src, int m, uint64_t *bar) {
+    const uintptr_t A = (uintptr_t)src, E = A + (uintptr_t)m * sizeof(T);
+    const uintptr_t A16 = (A + 15) & ~(uintptr_t)15, E16 = E & ~(uintptr_t)15;
+    T *st = (T *)(area + (A & 15));
+    const bool bulk = E16 > A16;
+    const int h = bulk ? (int)((A16 - A) / sizeof(T)) : m;  // head [0, h)
+    const int t0 = bulk ? (int)((E16 - A) / sizeof(T)) : m;  // tail [t0, m)
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(bar, bulk ? (uint32_t)(E16 - A16) : 0u);
+        if (bulk) bulk_g2s((unsigned char *)st + (A16 - A), (const void *)A16, (uint32_t)(E16 - A16), bar);
+    } else if (tid - 1 < h) {
+        st[tid - 1] = src[tid - 1];
+    } else if (tid - 1 - h < m - t0) {
+        st[t0 + tid - 1 - h] = src[t0 + tid - 1 - h];
+    }
+    return st;
+}
+
 template <int KK, int PB>
 __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, int64_t eidx, int cap, Entry *refine,
-                                             unsigned long long *refine_count, int fin_ins, long long *prof) {
+                                             unsigned long long *refine_count, int fin_ins, long long *prof,
+                                             uint64_t *bar, uint32_t &parity) {
 #define FIN_MARK(slot)                                                                                   \
     do {                                                                                                 \
         if (prof && threadIdx.x == 0) prof[eidx * 8 + (slot)] = clock64();                              \
@@ -1130,7 +1184,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     extern __shared__ __align__(16) unsigned char smem[];
     const FinLayout L = fin_layout(cap, PB);
     uint64_t *Bo = (uint64_t *)(smem + L.off_o);  // ordered key images, placed
-    P *PBf = (P *)(smem + L.off_pb);
     uint16_t *Ix = (uint16_t *)(smem + L.off_i);  // record index of each placed element
     uint32_t *cw = (uint32_t *)(smem + L.off_cur);  // 16-bit counters, two per word
     uint16_t *sst = (uint16_t *)(smem + L.off_st);
@@ -1150,14 +1203,22 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     P *op = (P *)B.out_p + e.start;
     const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
     const int base = w * 32 * F + lane;
+    // payload: staged in input order by the TMA, gathered by record index at
+    // the store (no registers held through the sort)
+    const P *pin = nullptr;
+    if constexpr (PB != 0) pin = stage_range<P>(smem + L.off_pb, sp, m, bar);
+    auto pay_wait = [&]() {
+        if constexpr (PB != 0) {
+            mbar_wait(bar, parity);
+            parity ^= 1u;
+        }
+    };
 
     uint64_t o[F];
-    P pay[F];
 #pragma unroll
     for (int j = 0; j < F; j++) {
         const int i = base + j * 32;
         o[j] = i < m ? sk[i] : 0ull;
-        if constexpr (PB != 0) pay[j] = i < m ? sp[i] : (P)0;
     }
     if (tid == 0) nbig = 0;
     bool anyneg = false;
@@ -1205,13 +1266,14 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         return kb;
     };
     if (omin == omax) {  // all equal: already in stable order
+        pay_wait();
         if (e.src != 2) {
 #pragma unroll
             for (int j = 0; j < F; j++) {
                 const int i = base + j * 32;
                 if (i < m) {
                     ok[i] = key_bits(o[j], i);
-                    if constexpr (PB != 0) op[i] = pay[j];
+                    if constexpr (PB != 0) op[i] = pin[i];
                 }
             }
         }
@@ -1334,7 +1396,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             const uint32_t pos = (old >> (16 * (d & 1))) & 0xFFFFu;
             Bo[pos] = o[j];
             Ix[pos] = (uint16_t)(base + j * 32);
-            if constexpr (PB != 0) PBf[pos] = pay[j];
         }
     }
     if (nb > 0) {
@@ -1399,10 +1460,10 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
                 const uint32_t pos = b0 + __popc(peers & lt);
                 Bo[pos] = o[j];
                 Ix[pos] = (uint16_t)(base + j * 32);
-                if constexpr (PB != 0) PBf[pos] = pay[j];
             }
         }
     }
+    pay_wait();
     __syncthreads();
     FIN_MARK(4);
     // ---- rank inside each sub-bucket by (key, record index) and store to
@@ -1431,7 +1492,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             }
         }
         ok[a + rank] = key_bits(ov, idx);
-        if constexpr (PB != 0) op[a + rank] = PBf[i];
+        if constexpr (PB != 0) op[a + rank] = pin[idx];
     }
     FIN_MARK(5);
     FIN_MARK(6);
@@ -1446,10 +1507,14 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
                                                   Entry *refine, unsigned long long *refine_count, int fin_ins,
                                                   long long *prof, unsigned long long *ticket) {
     __shared__ long long next;
+    __shared__ uint64_t bar;  // payload staging (TMA bulk copy) completion
+    uint32_t parity = 0;
     const int64_t ne = count ? (int64_t)*count : count_const;
+    if (PB != 0 && threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
     if (!ticket) {  // one run per CTA (grid = exact count)
         if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
-                                                           fin_ins, prof);
+                                                           fin_ins, prof, &bar, parity);
         return;
     }
     while (true) {  // dynamic scheduling: a CTA takes the next run as soon as it is free
@@ -1457,7 +1522,7 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
         __syncthreads();
         const int64_t i = next;
         if (i >= ne) break;
-        finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof);
+        finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof, &bar, parity);
         __syncthreads();
     }
 }

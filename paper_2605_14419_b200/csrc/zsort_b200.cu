@@ -17,6 +17,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <unordered_map>
 
 #include "../../include/zsort_b200.h"
 #include "dist_kernels.cuh"
@@ -217,7 +219,24 @@ Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
 
 template <typename F>
 void smem_optin(F *func, size_t bytes) {
-    if (bytes > 48 * 1024) cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    // Raise the kernel's dynamic shared-memory cap once to the largest value it
+    // can take (device opt-in maximum minus its static shared memory), not to
+    // `bytes`: concurrent callers on other host threads then never lower the
+    // cap under a launch in flight.  The attribute is a cap, it reserves nothing.
+    if (bytes <= 48 * 1024) return;
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void *key = (const void *)((uintptr_t)(const void *)func ^ ((uintptr_t)dev << 56));
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(key)) return;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, func);
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    done[key] = 1;
 }
 
 __global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t *wfirst, int64_t nwin, int64_t n, int64_t k,
@@ -472,7 +491,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         {
             PhaseScope ph(PH_MOMENTS, c.st, 2);
             k_fine_hist<KK><<<num_sms() * 2, 512, (size_t)KF_MAX * 4, c.st>>>(c.B.in_k, n, seg_cur, KF_MAX, fine);
-            k_build_cdf<<<1, 1024, 0, c.st>>>(fine, KF_MAX, n, seg_cur, (double *)(c.ws + c.L.lut));
+            k_build_cdf<<<1, 1024, 0, c.st>>>(fine, KF_MAX, n, seg_cur, (float2 *)(c.ws + c.L.lut));
         }
         ZSB_LAUNCH("k_fine_hist/k_build_cdf");
     }
@@ -775,7 +794,7 @@ int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32
     ctx.B.out_k = (uint64_t *)d_out_keys;
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = nullptr;
-    ctx.B.cdf = (const double *)(ctx.ws + ctx.L.lut);
+    ctx.B.cdf = (const float2 *)(ctx.ws + ctx.L.lut);
     return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats);
 }
 
