@@ -104,6 +104,8 @@ enum Ctrl {
     C_NREF1 = 15,
     C_FTICK0 = 16,  // finish work tickets (dynamic scheduling), one per launch in a pair
     C_FTICK1 = 17,
+    C_SAMP_TICKET = 18,  // sampled level-1 kernels
+    C_SAMPLE_OK = 19,    // 1: level 1 mapped from the sample (exact K1 skipped)
     C_SLOTS = 24
 };
 

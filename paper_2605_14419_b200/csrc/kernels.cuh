@@ -177,6 +177,7 @@ template <int KK>
 __global__ void __launch_bounds__(NT) k_moments(const uint64_t *__restrict__ keys, int64_t n,
                                                 MomPartial *__restrict__ parts, unsigned long long *ctrl,
                                                 SegParams *seg, MapCfg mc, double *h_dbg) {
+    if (ctrl[C_SAMPLE_OK]) return;  // level 1 already mapped from the sample
     const double c0 = key_value<KK>(keys[0]);
     unsigned long long omin = ~0ull, omax = 0, slo = 0, nan = 0;
     long long shi = 0;
@@ -385,7 +386,7 @@ constexpr int HT = 1024;  // threads of the histogram kernel (one tile per CTA)
 
 template <int KK>
 __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                             uint32_t *__restrict__ mat) {
+                                             uint32_t *__restrict__ mat, unsigned long long *status) {
     extern __shared__ uint32_t hist[];
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
@@ -404,15 +405,26 @@ __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restr
     __syncthreads();
     const uint64_t *src = src_keys(B, p.src);
     int64_t i = t0 + threadIdx.x;
+    // a sampled level 1 (MODE_ZCDF) has not screened the input for NaN: K2 does
+    const bool screen = KK == KEY_F64 && p.mode == MODE_ZCDF && p.level == 1;
+    bool nan = false;
+    auto is_nan = [](uint64_t b) { return (b << 1) > 0xFFE0000000000000ull; };
     for (; i + 7 * HT < t1; i += 8 * HT) {
         uint64_t b[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
 #pragma unroll
-        for (int u = 0; u < 8; u++) atomicAdd(&hist[seg_bucket<KK>(b[u], p, i + u * HT, B.cuts, cdf)], 1u);
+        for (int u = 0; u < 8; u++) {
+            if (screen) nan |= is_nan(b[u]);
+            atomicAdd(&hist[seg_bucket<KK>(b[u], p, i + u * HT, B.cuts, cdf)], 1u);
+        }
     }
-    for (; i < t1; i += HT) atomicAdd(&hist[seg_bucket<KK>(__ldcs(src + i), p, i, B.cuts, cdf)], 1u);
-    __syncthreads();
+    for (; i < t1; i += HT) {
+        const uint64_t b = __ldcs(src + i);
+        if (screen) nan |= is_nan(b);
+        atomicAdd(&hist[seg_bucket<KK>(b, p, i, B.cuts, cdf)], 1u);
+    }
+    if (__syncthreads_or(nan) && threadIdx.x == 0) *status = 3;  // ZSB_ERR_NAN
     for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
 }
 
@@ -843,19 +855,23 @@ __global__ void __launch_bounds__(512) k_fine_hist(const uint64_t *__restrict__ 
 }
 
 // Knot pairs (cdf[s], cdf[s+1]) of the piecewise-linear CDF in bucket units
-// (fp32: rounding is monotone, so the knots stay non-decreasing) and the
-// switch of the level-1 segment to MODE_ZCDF.
-__global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restrict__ counts, int kf, int64_t n,
-                                                    SegParams *seg, float2 *cdf) {
-    __shared__ unsigned long long wsum[32];
+// (fp32: rounding is monotone, so the knots stay non-decreasing) from the
+// coarse-bin counts (summing to `total`), and the switch of the level-1
+// segment to MODE_ZCDF.  One CTA of NTHR threads; NTHR divides kf.
+template <int NTHR>
+__device__ void build_cdf_block(const unsigned int *counts, int kf, int64_t total, SegParams *seg, SegParams p,
+                                float za, float zb, float2 *cdf) {
+    constexpr int PER_MAX = KF_MAX / NTHR;
+    __shared__ unsigned long long wsum[NTHR / 32];
     __shared__ float knot[KF_MAX + 1];
-    SegParams p = *seg;
-    float za, zb;
-    if (p.mode != MODE_ZSCORE || !zc_coeffs(p, kf, za, zb)) return;
-    const int per = kf / 1024;  // kf is a multiple of 1024
+    const int per = kf / NTHR;
     const int f0 = threadIdx.x * per;
+    unsigned int cv[PER_MAX];
     unsigned long long tsum = 0;
-    for (int q = 0; q < per; q++) tsum += counts[f0 + q];
+#pragma unroll
+    for (int q = 0; q < PER_MAX; q++) cv[q] = q < per ? __ldcg(&counts[f0 + q]) : 0u;
+#pragma unroll
+    for (int q = 0; q < PER_MAX; q++) tsum += cv[q];
     unsigned long long x = tsum;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int o = 1; o < 32; o <<= 1) {
@@ -866,14 +882,17 @@ __global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restri
     __syncthreads();
     unsigned long long run = x - tsum;
     for (int q = 0; q < w; q++) run += wsum[q];
-    const double inv = (double)p.k / (double)n;  // knots in bucket units
-    for (int q = 0; q < per; q++) {
-        knot[f0 + q] = (float)((double)run * inv);
-        run += counts[f0 + q];
+    const double inv = (double)p.k / (double)total;  // knots in bucket units
+#pragma unroll
+    for (int q = 0; q < PER_MAX; q++) {
+        if (q < per) {
+            knot[f0 + q] = (float)((double)run * inv);
+            run += cv[q];
+        }
     }
-    if (threadIdx.x == 1023) knot[kf] = (float)p.k;
+    if (threadIdx.x == NTHR - 1) knot[kf] = (float)p.k;
     __syncthreads();
-    for (int s = threadIdx.x; s < kf; s += 1024) cdf[s] = make_float2(knot[s], knot[s + 1]);
+    for (int s = threadIdx.x; s < kf; s += NTHR) cdf[s] = make_float2(knot[s], knot[s + 1]);
     if (threadIdx.x == 0) {
         p.scale = p.scale * ((double)kf / (double)p.k);
         p.kf = kf;
@@ -882,6 +901,179 @@ __global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restri
         p.mode = MODE_ZCDF;
         *seg = p;
     }
+}
+
+__global__ void __launch_bounds__(1024) k_build_cdf(const unsigned int *__restrict__ counts, int kf, int64_t n,
+                                                    SegParams *seg, float2 *cdf) {
+    SegParams p = *seg;
+    float za, zb;
+    if (p.mode != MODE_ZSCORE || !zc_coeffs(p, kf, za, zb)) return;
+    build_cdf_block<1024>(counts, kf, n, seg, p, za, zb, cdf);
+}
+
+// ---------------------------------------------------- sampled level 1
+// Fitted mapping: the coarse z-coordinate and its CDF only need to be
+// monotone, not exact, so level 1 takes them from a stratified sample --
+// SAMP_CHUNKS_MAX evenly spaced runs of SAMP_CHUNK consecutive keys (every key
+// when n <= ~256K) -- instead of two full passes over the input.  The first
+// full pass is then K2's histogram, which also raises the NaN status.  A
+// degenerate sample (NaN, all equal, no finite spread) leaves the segment in
+// z-score mode with C_SAMPLE_OK = 0 and the exact K1 path runs instead.
+
+constexpr int SAMP_CHUNK = 32;
+constexpr int SAMP_CHUNKS_MAX = 8192;
+constexpr int SAMP_UNROLL = 8;  // sample keys per thread, loads issued together (grid = sample / (NT * 8))
+
+struct SampPartial {
+    unsigned long long omin, omax, nan, pad;
+    double s1, s2, cnt, pad2;
+};
+
+// position of sample item g (chunk g / SAMP_CHUNK, offset g % SAMP_CHUNK), -1 past a short chunk
+__device__ __forceinline__ int64_t sample_pos(int64_t g, int64_t nitems, int64_t stride, int64_t clen) {
+    const int64_t off = g & (SAMP_CHUNK - 1);
+    return (g < nitems && off < clen) ? (g / SAMP_CHUNK) * stride + off : -1;
+}
+
+template <int KK>
+__global__ void __launch_bounds__(NT) k_sample_moments(const uint64_t *__restrict__ keys, int64_t n,
+                                                       int64_t nchunks, int64_t stride, SampPartial *parts,
+                                                       unsigned long long *ctrl, SegParams *seg, int kf) {
+    const double c0 = key_value<KK>(keys[0]);
+    const int64_t clen = stride < SAMP_CHUNK ? stride : SAMP_CHUNK;
+    const int64_t nitems = nchunks * SAMP_CHUNK, gstride = (int64_t)gridDim.x * NT;
+    unsigned long long omin = ~0ull, omax = 0, nan = 0;
+    double s1 = 0.0, s2 = 0.0, cnt = 0.0;
+    for (int64_t g0 = (int64_t)blockIdx.x * NT + threadIdx.x; g0 < nitems; g0 += SAMP_UNROLL * gstride) {
+        uint64_t b[SAMP_UNROLL];
+        bool v[SAMP_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SAMP_UNROLL; u++) {
+            const int64_t i = sample_pos(g0 + u * gstride, nitems, stride, clen);
+            v[u] = i >= 0;
+            b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < SAMP_UNROLL; u++) {
+            if (!v[u]) continue;
+            const double x = key_value<KK>(b[u]);
+            if (KK == KEY_F64 && x != x) {
+                nan++;
+                continue;
+            }
+            const uint64_t o = ord_key<KK>(b[u]);
+            omin = o < omin ? o : omin;
+            omax = o > omax ? o : omax;
+            const double d = x - c0;
+            s1 += d;
+            s2 += d * d;
+            cnt += 1.0;
+        }
+    }
+    __shared__ SampPartial wp[NWARPS];
+    __shared__ bool last;
+    const int w = threadIdx.x >> 5, lane = lane_id();
+    auto block_reduce = [&]() {  // warp shuffles, then warp 0 over the warp partials
+        omin = warp_min_u64(omin);
+        omax = warp_max_u64(omax);
+        nan = warp_sum(nan);
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        cnt = warp_sum(cnt);
+        if (lane == 0) wp[w] = SampPartial{omin, omax, nan, 0, s1, s2, cnt, 0.0};
+        __syncthreads();
+        if (w == 0) {
+            SampPartial a = lane < NWARPS ? wp[lane] : SampPartial{~0ull, 0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+            omin = warp_min_u64(a.omin);
+            omax = warp_max_u64(a.omax);
+            nan = warp_sum(a.nan);
+            s1 = warp_sum(a.s1);
+            s2 = warp_sum(a.s2);
+            cnt = warp_sum(a.cnt);
+        }
+    };
+    block_reduce();
+    if (threadIdx.x == 0) {
+        parts[blockIdx.x] = SampPartial{omin, omax, nan, 0, s1, s2, cnt, 0.0};
+        __threadfence();
+        last = atomicAdd(&ctrl[C_SAMP_TICKET], 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    omin = ~0ull, omax = 0, nan = 0, s1 = 0.0, s2 = 0.0, cnt = 0.0;
+    for (int j = threadIdx.x; j < (int)gridDim.x; j += NT) {
+        const unsigned long long qmin = __ldcg(&parts[j].omin), qmax = __ldcg(&parts[j].omax);
+        omin = qmin < omin ? qmin : omin;
+        omax = qmax > omax ? qmax : omax;
+        nan += __ldcg(&parts[j].nan);
+        s1 += __ldcg(&parts[j].s1);
+        s2 += __ldcg(&parts[j].s2);
+        cnt += __ldcg(&parts[j].cnt);
+    }
+    __syncthreads();  // wp reuse
+    block_reduce();
+    if (threadIdx.x != 0) return;
+    ctrl[C_SAMP_TICKET] = 0;
+    ctrl[C_SAMPLE_OK] = 0;
+    if (nan || cnt < 2.0 || omin == omax) return;  // exact K1 decides (NaN status, copy, integer)
+    const double mean = c0 + s1 / cnt;
+    const double dm = mean - c0;
+    double m2 = s2 - 2.0 * dm * s1 + cnt * dm * dm;
+    if (m2 < 0.0) m2 = 0.0;
+    const double sd = sqrt(m2 / cnt);
+    const double vmin = key_value<KK>(key_from_ord<KK>(omin)), vmax = key_value<KK>(key_from_ord<KK>(omax));
+    const double span = (vmax - vmin) / sd;
+    if (!(sd > 0.0) || !isfinite(sd) || !(span > 0.0) || !isfinite(span)) return;
+    SegParams p = *seg;
+    p.center = mean;
+    p.std = sd;
+    p.zmin = (mean - vmin) / sd;
+    p.scale = ((double)p.k * (1.0 - 0x1p-20)) / span;
+    float za, zb;
+    if (!isfinite(p.zmin) || !(p.scale > 0.0) || !isfinite(p.scale) || !zc_coeffs(p, kf, za, zb)) return;
+    p.za = za;
+    p.zb = zb;
+    *seg = p;
+    ctrl[C_SAMPLE_OK] = 1;
+}
+
+template <int KK>
+__global__ void __launch_bounds__(NT) k_sample_cdf(const uint64_t *__restrict__ keys, int64_t n, int64_t nchunks,
+                                                   int64_t stride, unsigned int *fine, unsigned long long *ctrl,
+                                                   SegParams *seg, int kf, float2 *cdf) {
+    if (!ctrl[C_SAMPLE_OK]) return;
+    __shared__ uint32_t fh[KF_MAX];
+    __shared__ bool last;
+    const SegParams p = *seg;
+    const int64_t clen = stride < SAMP_CHUNK ? stride : SAMP_CHUNK;
+    const int64_t nitems = nchunks * SAMP_CHUNK, gstride = (int64_t)gridDim.x * NT;
+    for (int b = threadIdx.x; b < kf; b += NT) fh[b] = 0;
+    __syncthreads();
+    for (int64_t g0 = (int64_t)blockIdx.x * NT + threadIdx.x; g0 < nitems; g0 += SAMP_UNROLL * gstride) {
+        uint64_t b[SAMP_UNROLL];
+        bool v[SAMP_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SAMP_UNROLL; u++) {
+            const int64_t i = sample_pos(g0 + u * gstride, nitems, stride, clen);
+            v[u] = i >= 0;
+            b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < SAMP_UNROLL; u++)
+            if (v[u]) atomicAdd(&fh[zc_bin(zc_coord(key_value<KK>(b[u]), p.center, p.za, p.zb), kf)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kf; b += NT)
+        if (fh[b]) atomicAdd(&fine[b], fh[b]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&ctrl[C_SAMP_TICKET], 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) ctrl[C_SAMP_TICKET] = 0;
+    build_cdf_block<NT>(fine, kf, nchunks * clen, seg, p, p.za, p.zb, cdf);  // no NaN in the sample
 }
 
 // ------------------------------------------------------------ classify

@@ -320,7 +320,7 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     smem_optin(k_hist<KK>, kbytes);
     {
         PhaseScope ph(PH_HIST, c.st);
-        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat);
+        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS);
     }
     ZSB_LAUNCH("k_hist");
     int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
@@ -477,6 +477,22 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                                          1.0, 0.0, 1.0, MODE_ZSCORE);
     }
     ZSB_LAUNCH("k_init_level1");
+    const bool equalize = cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0);
+    unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
+    if (equalize) ZSB_CUDA(cudaMemsetAsync(fine, 0, (size_t)KF_MAX * 4, c.st));
+    if (equalize && !env_int("ZSB_NO_SAMPLE", 0)) {
+        // sampled level-1 mapping; on a degenerate sample the exact K1 path below runs
+        const int64_t nchunks = std::min<int64_t>(SAMP_CHUNKS_MAX, (n + SAMP_CHUNK - 1) / SAMP_CHUNK);
+        const int64_t stride = n / nchunks;
+        const int sgrid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)num_sms() * MOM_GRID_PER_SM,
+                                 (nchunks * SAMP_CHUNK + NT * SAMP_UNROLL - 1) / (NT * SAMP_UNROLL)));
+        PhaseScope ph(PH_MOMENTS, c.st, 2);
+        k_sample_moments<KK><<<sgrid, NT, 0, c.st>>>(c.B.in_k, n, nchunks, stride, (SampPartial *)(c.ws + c.L.parts),
+                                                     ctrl, seg_cur, KF_MAX);
+        k_sample_cdf<KK><<<sgrid, NT, 0, c.st>>>(c.B.in_k, n, nchunks, stride, fine, ctrl, seg_cur, KF_MAX,
+                                                 (float2 *)(c.ws + c.L.lut));
+    }
     int grid = std::max(1, std::min<int>(num_sms() * MOM_GRID_PER_SM, (int)((n + NT - 1) / NT)));
     {
         PhaseScope ph(PH_MOMENTS, c.st);
@@ -484,10 +500,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                                              nullptr);
     }
     ZSB_LAUNCH("k_moments");
-    if (cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0)) {
-        // histogram equalisation of level 1 (acts only if K1 chose z-score mode)
-        unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
-        ZSB_CUDA(cudaMemsetAsync(fine, 0, (size_t)KF_MAX * 4, c.st));
+    if (equalize) {
+        // exact histogram equalisation of level 1 (acts only if K1 ran and chose z-score mode)
         {
             PhaseScope ph(PH_MOMENTS, c.st, 2);
             k_fine_hist<KK><<<num_sms() * 2, 512, (size_t)KF_MAX * 4, c.st>>>(c.B.in_k, n, seg_cur, KF_MAX, fine);
@@ -844,10 +858,12 @@ int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double
     size_t kb = (size_t)k * 4;
     if (key_dtype == ZSB_KEY_I64) {
         smem_optin(k_hist<0>, kb);
-        k_hist<0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
+        k_hist<0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
+                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS);
     } else {
         smem_optin(k_hist<1>, kb);
-        k_hist<1><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat);
+        k_hist<1><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
+                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS);
     }
     ZSB_LAUNCH("k_hist");
     k_bucket_totals<<<(unsigned)((k + 255) / 256), 256, 0, ctx.st>>>(mat, k, ctx.P.ntiles, d_counts);
