@@ -10,7 +10,7 @@
 // The stable partition to destination ranks reuses K2/K3/K4 in MODE_DEST.
 #pragma once
 
-#include "kernels.cuh"
+#include "sort_kernels.cuh"
 
 namespace zsb {
 

@@ -1,4 +1,4 @@
-// kernels.cuh -- sm_100a kernels of the stable z-score partitioning sort.
+// sort_kernels.cuh -- sm_100a kernels of the stable z-score partitioning sort.
 //
 //  K1  k_moments        grid-wide fp64 moments + exact int sum -> level-1 params
 //  K1s k_seg_moments    per-segment min/max/squared deviation (recursion levels)
@@ -518,14 +518,17 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 // starts from its column of the scanned count matrix, so tiles land in
 // input order inside every bucket.  The tile is processed in rounds of
 // NT*ITEMS records; each round is stably sorted by bucket in shared memory:
-//   count  warp w owns the contiguous slice [w*32*ITEMS, (w+1)*32*ITEMS) of
-//          the round; equal-bucket keys are ranked with __match_any_sync and
-//          the leaders advance per-(bucket, warp) u16 counters;
+//   count  warp w owns the slice [w*32*ITEMS, (w+1)*32*ITEMS) of the round
+//          (item j of lane l = record w*32*ITEMS + j*32 + l); every item takes
+//          a rank from its per-(warp, bucket) u16 counter with one shared
+//          atomic (ranks follow j; lane ties inside one instruction are
+//          fixed at the write);
 //   scan   exclusive scan of the counters in (bucket, warp) order;
-//   place  records go to shared memory at their stable local position;
-//   write  thread i stores staged record i to cursor[b] + (i - run_start[b]):
-//          consecutive threads write consecutive addresses of each bucket run
-//          (coalesced), then the bucket cursors advance by the run lengths.
+//   place  records go to shared memory at (warp, bucket) base + rank;
+//   write  thread i stores staged record i to cursor[b] + (i - run_start[b])
+//          (tie groups reordered by lane): consecutive threads write
+//          consecutive addresses of each bucket run (coalesced), then the
+//          bucket cursors advance by the run lengths.
 // Every record keeps its input order within its bucket, the front-to-back
 // semantics of scatter_pass (_kernels.py:124-133), with no cross-warp
 // serialization.
@@ -563,7 +566,7 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
     o += (size_t)round * pb;
     o = (o + 15) & ~(size_t)15;
     L.off_b = o;
-    o += (size_t)round * 2;
+    o += (size_t)round * 4;
     o = (o + 15) & ~(size_t)15;
     L.off_cdf = o;  // the CDF table (level-1 equalisation only) follows the layout
     L.total = o;
@@ -708,7 +711,7 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     uint16_t *lst = (uint16_t *)(smem + L.off_lst);
     uint64_t *stk = (uint64_t *)(smem + L.off_k);
     P *stp = (P *)(smem + L.off_p);
-    uint16_t *stb = (uint16_t *)(smem + L.off_b);
+    uint32_t *stb = (uint32_t *)(smem + L.off_b);  // bucket | record index in the round << 16
     float2 *cdf = (float2 *)(smem + L.off_cdf);
     if (p.mode == MODE_ZCDF)
         for (int q = threadIdx.x; q < p.kf; q += ST) cdf[q] = B.cdf[q];
@@ -722,7 +725,6 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     __syncthreads();
 
     const int w = threadIdx.x >> 5, lane = lane_id();
-    const unsigned lt = lanemask_lt();
     // Software pipeline: the keys of round r+1 are loaded right after round
     // r's placement (key[] is free then) and land during its write phase;
     // payload loads are issued at the start of a round and consumed only at
@@ -747,48 +749,41 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         for (int j = 0; j < ITEMS; j++)
             bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
         SCAT_MARK(0);  // loads + bucket ids
-        // count per (warp, bucket): all MATCH.ANY issued back to back, the
-        // leaders add with shared atomics on the containing 32-bit word.  What
-        // placement needs of an item is packed into one word (bucket 11 bits,
-        // leader lane 5, rank among its warp peers 5, peer count 6) so the
-        // round keeps one register per item besides its key and payload.
-        uint32_t pk[ITEMS];
+        // count: one shared atomic per item on its per-(warp, bucket) u16
+        // counter; the returned count is the item's rank among its warp's
+        // items of that bucket.  A warp's atomics reach shared memory in
+        // program order, so ranks follow j (input order); only lanes of one
+        // instruction that share a bucket (a "tie group", ~0.5 per warp
+        // instruction at k = 1024) may be ranked out of lane order -- they get
+        // consecutive ranks and are reordered by lane at the write.  This
+        // replaces __match_any_sync, whose cost grows with the number of
+        // distinct buckets in the warp.
+        uint32_t pk[ITEMS];  // bucket | rank << 16
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const unsigned m = __match_any_sync(0xffffffffu, bk[j]);
-            pk[j] = bk[j] < 0 ? 0xffffffffu
-                              : (uint32_t)bk[j] | ((uint32_t)(__ffs(m) - 1) << 11) | ((uint32_t)__popc(m & lt) << 16) |
-                                    ((uint32_t)__popc(m) << 21);
-        }
-#pragma unroll
-        for (int j = 0; j < ITEMS; j++) {
-            if (pk[j] != 0xffffffffu && ((pk[j] >> 16) & 31) == 0) {
-                const int q = w * k + (int)(pk[j] & 2047);
-                atomicAdd((uint32_t *)cnt + (q >> 1), (pk[j] >> 21) << (16 * (q & 1)));
+            if (bk[j] >= 0) {
+                const int q = w * k + bk[j];
+                const uint32_t sh = 16 * (q & 1);
+                const uint32_t old = atomicAdd((uint32_t *)cnt + (q >> 1), 1u << sh);
+                pk[j] = (uint32_t)bk[j] | (((old >> sh) & 0xFFFFu) << 16);
+            } else {
+                pk[j] = 0xffffffffu;
             }
         }
         __syncthreads();
-        SCAT_MARK(1);  // match + counting
+        SCAT_MARK(1);  // counting
         scan_wd<SW>(cnt, k, lst, wtot);
         SCAT_MARK(2);  // scan
-        // place (stable local sort by bucket): items in input order
+        // place: slot = (warp, bucket) base + rank; the slot remembers the
+        // bucket and the record's index in the round
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const bool valid = pk[j] != 0xffffffffu;
-            const int leader = valid ? (int)((pk[j] >> 11) & 31) : lane;
-            const int b = (int)(pk[j] & 2047);
-            uint32_t b0 = 0;
-            if (valid && lane == leader) {
-                b0 = cnt[w * k + b];
-                cnt[w * k + b] = (uint16_t)(b0 + (pk[j] >> 21));
-            }
-            __syncwarp();
-            b0 = __shfl_sync(0xffffffffu, b0, leader);
-            if (valid) {
-                const uint32_t pos = b0 + ((pk[j] >> 16) & 31);
+            if (pk[j] != 0xffffffffu) {
+                const int b = (int)(pk[j] & 0xFFFFu);
+                const uint32_t pos = (uint32_t)cnt[w * k + b] + (pk[j] >> 16);
                 stk[pos] = key[j];
                 if constexpr (PB != 0) stp[pos] = pay[j];
-                stb[pos] = (uint16_t)b;
+                stb[pos] = (uint32_t)b | ((uint32_t)(base + j * 32) << 16);
             }
         }
         __syncthreads();
@@ -799,10 +794,24 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
 #pragma unroll
             for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nvn ? __ldcs(sk + rn + base + j * 32) : 0ull;
         }
-        // coalesced run writes, counters reset for the next round
+        // coalesced run writes; a slot whose neighbour is in its tie group
+        // (same bucket, same warp and item j: index bits above the lane)
+        // takes its lane-ordered place inside the group's slot range
         for (int i = threadIdx.x; i < nvalid; i += ST) {
-            const int b = stb[i];
-            const uint32_t dst = cur[b] + (uint32_t)(i - lst[b]);
+            const uint32_t e = stb[i];
+            const int b = (int)(e & 0xFFFFu);
+            auto same = [&](uint32_t x) { return ((x ^ e) & 0xFFE0FFFFu) == 0u; };
+            int r = i - (int)lst[b];
+            if ((i > 0 && same(stb[i - 1])) || (i + 1 < nvalid && same(stb[i + 1]))) {
+                int g0 = i, g1 = i + 1;
+                while (g0 > 0 && same(stb[g0 - 1])) g0--;
+                while (g1 < nvalid && same(stb[g1])) g1++;
+                const uint32_t me = (e >> 16) & 31u;
+                int c = 0;
+                for (int x = g0; x < g1; x++) c += ((stb[x] >> 16) & 31u) < me;
+                r = g0 + c - (int)lst[b];
+            }
+            const uint32_t dst = cur[b] + (uint32_t)r;
             dk[dst] = stk[i];
             if constexpr (PB != 0) dp[dst] = stp[i];
         }

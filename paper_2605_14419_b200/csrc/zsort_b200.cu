@@ -22,7 +22,7 @@
 
 #include "../../include/zsort_b200.h"
 #include "dist_kernels.cuh"
-#include "kernels.cuh"
+#include "sort_kernels.cuh"
 
 using namespace zsb;
 
@@ -332,7 +332,9 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     }
     ZSB_LAUNCH("k_scan");
     const size_t cdf_bytes = (c.B.cdf && segs_level1) ? (size_t)(CDF_KNOTS + 1) * 8 : 0;
-    if (scat_warps(kmax, env_int("ZSB_SW16_ABOVE", 512)) == 8) {
+    const bool sw16 = scat_warps(kmax, env_int("ZSB_SW16_ABOVE", 512)) == 16 &&
+                      scat_layout(kmax, PB, 16).total + cdf_bytes <= (size_t)227 * 1024 - 1024;
+    if (!sw16) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 8>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);

@@ -71,7 +71,7 @@ class GlobalParams:
 
 def plan_params(count: float, s1: float, s2: float, shift: float, vmin: float, vmax: float, k: int) -> GlobalParams:
     """Fitted Eq. 1 parameters from allreduced moments (finalize_params in
-    kernels.cuh, fitted branch).  Degenerate inputs map every key to bucket
+    sort_kernels.cuh, fitted branch).  Degenerate inputs map every key to bucket
     0, which is still correct (no cut can then fall inside a non-constant
     bucket), only unbalanced."""
     mean = shift + s1 / count

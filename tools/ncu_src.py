@@ -6,10 +6,6 @@ rep, pat = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{pat}", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout.splitlines()
-import os
-_c = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2605_14419_b200", "csrc")
-KLINES = open(os.path.join(_c, "kernels.cuh")).read().splitlines()
-DIST_LINES = len(open(os.path.join(_c, "dist_kernels.cuh")).read().splitlines())
 res, fname, hdr, seen_fn = [], None, None, set()
 for l in out:
     if l.startswith('"File Path"'):
@@ -30,8 +26,6 @@ for l in out:
         continue
     try:
         txt = r[1]
-        if fname == "dist_kernels.cuh" and int(r[0]) > DIST_LINES:  # ncu folds kernels.cuh into its includer
-            txt = "[kernels.cuh] " + KLINES[int(r[0]) - 1] if int(r[0]) <= len(KLINES) else txt
         res.append((int(r[4] or 0), int(float(r[7] or 0)), fname, r[0], txt[:110]))
     except (ValueError, IndexError):
         pass
