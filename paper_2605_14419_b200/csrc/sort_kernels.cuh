@@ -522,13 +522,12 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 //          (item j of lane l = record w*32*ITEMS + j*32 + l); every item takes
 //          a rank from its per-(warp, bucket) u16 counter with one shared
 //          atomic (ranks follow j; lane ties inside one instruction are
-//          fixed at the write);
+//          detected by re-reading the counter and re-ranked by a match);
 //   scan   exclusive scan of the counters in (bucket, warp) order;
 //   place  records go to shared memory at (warp, bucket) base + rank;
-//   write  thread i stores staged record i to cursor[b] + (i - run_start[b])
-//          (tie groups reordered by lane): consecutive threads write
-//          consecutive addresses of each bucket run (coalesced), then the
-//          bucket cursors advance by the run lengths.
+//   write  thread i stores staged record i to cursor[b] + (i - run_start[b]):
+//          consecutive threads write consecutive addresses of each bucket run
+//          (coalesced), then the bucket cursors advance by the run lengths.
 // Every record keeps its input order within its bucket, the front-to-back
 // semantics of scatter_pass (_kernels.py:124-133), with no cross-warp
 // serialization.
@@ -566,7 +565,7 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
     o += (size_t)round * pb;
     o = (o + 15) & ~(size_t)15;
     L.off_b = o;
-    o += (size_t)round * 4;
+    o += (size_t)round * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_cdf = o;  // the CDF table (level-1 equalisation only) follows the layout
     L.total = o;
@@ -711,7 +710,7 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     uint16_t *lst = (uint16_t *)(smem + L.off_lst);
     uint64_t *stk = (uint64_t *)(smem + L.off_k);
     P *stp = (P *)(smem + L.off_p);
-    uint32_t *stb = (uint32_t *)(smem + L.off_b);  // bucket | record index in the round << 16
+    uint16_t *stb = (uint16_t *)(smem + L.off_b);
     float2 *cdf = (float2 *)(smem + L.off_cdf);
     if (p.mode == MODE_ZCDF)
         for (int q = threadIdx.x; q < p.kf; q += ST) cdf[q] = B.cdf[q];
@@ -751,31 +750,40 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         SCAT_MARK(0);  // loads + bucket ids
         // count: one shared atomic per item on its per-(warp, bucket) u16
         // counter; the returned count is the item's rank among its warp's
-        // items of that bucket.  A warp's atomics reach shared memory in
+        // items of that bucket.  A warp's shared-memory operations execute in
         // program order, so ranks follow j (input order); only lanes of one
-        // instruction that share a bucket (a "tie group", ~0.5 per warp
-        // instruction at k = 1024) may be ranked out of lane order -- they get
-        // consecutive ranks and are reordered by lane at the write.  This
-        // replaces __match_any_sync, whose cost grows with the number of
-        // distinct buckets in the warp.
+        // instruction that share a bucket (a tie group) may be ranked out of
+        // lane order.  Re-reading the counter right after the atomic exposes
+        // them (a member that is not its group's last sees the counter move by
+        // more than its own increment); only then does the warp pay for
+        // __match_any_sync, and the group is re-ranked in lane order from its
+        // end value.  Random keys tie in ~40% of instructions (k = 1024),
+        // sorted runs in all of them but with few distinct buckets, where the
+        // match is cheap.
         uint32_t pk[ITEMS];  // bucket | rank << 16
+        const unsigned lt = lanemask_lt();
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
+            uint32_t old = 0, after = 0;
+            const int q = w * k + (bk[j] < 0 ? 0 : bk[j]);
+            const uint32_t sh = 16 * (q & 1);
+            uint32_t *word = (uint32_t *)cnt + (q >> 1);
             if (bk[j] >= 0) {
-                const int q = w * k + bk[j];
-                const uint32_t sh = 16 * (q & 1);
-                const uint32_t old = atomicAdd((uint32_t *)cnt + (q >> 1), 1u << sh);
-                pk[j] = (uint32_t)bk[j] | (((old >> sh) & 0xFFFFu) << 16);
-            } else {
-                pk[j] = 0xffffffffu;
+                old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
+                after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
             }
+            const bool tie = bk[j] >= 0 && after != old + 1u;
+            if (__any_sync(0xffffffffu, tie)) {
+                const unsigned m = __match_any_sync(0xffffffffu, bk[j]);
+                if (bk[j] >= 0 && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
+            }
+            pk[j] = bk[j] >= 0 ? (uint32_t)bk[j] | (old << 16) : 0xffffffffu;
         }
         __syncthreads();
         SCAT_MARK(1);  // counting
         scan_wd<SW>(cnt, k, lst, wtot);
         SCAT_MARK(2);  // scan
-        // place: slot = (warp, bucket) base + rank; the slot remembers the
-        // bucket and the record's index in the round
+        // place: slot = (warp, bucket) base + rank
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
             if (pk[j] != 0xffffffffu) {
@@ -783,7 +791,7 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
                 const uint32_t pos = (uint32_t)cnt[w * k + b] + (pk[j] >> 16);
                 stk[pos] = key[j];
                 if constexpr (PB != 0) stp[pos] = pay[j];
-                stb[pos] = (uint32_t)b | ((uint32_t)(base + j * 32) << 16);
+                stb[pos] = (uint16_t)b;
             }
         }
         __syncthreads();
@@ -794,24 +802,10 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
 #pragma unroll
             for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nvn ? __ldcs(sk + rn + base + j * 32) : 0ull;
         }
-        // coalesced run writes; a slot whose neighbour is in its tie group
-        // (same bucket, same warp and item j: index bits above the lane)
-        // takes its lane-ordered place inside the group's slot range
+        // coalesced run writes
         for (int i = threadIdx.x; i < nvalid; i += ST) {
-            const uint32_t e = stb[i];
-            const int b = (int)(e & 0xFFFFu);
-            auto same = [&](uint32_t x) { return ((x ^ e) & 0xFFE0FFFFu) == 0u; };
-            int r = i - (int)lst[b];
-            if ((i > 0 && same(stb[i - 1])) || (i + 1 < nvalid && same(stb[i + 1]))) {
-                int g0 = i, g1 = i + 1;
-                while (g0 > 0 && same(stb[g0 - 1])) g0--;
-                while (g1 < nvalid && same(stb[g1])) g1++;
-                const uint32_t me = (e >> 16) & 31u;
-                int c = 0;
-                for (int x = g0; x < g1; x++) c += ((stb[x] >> 16) & 31u) < me;
-                r = g0 + c - (int)lst[b];
-            }
-            const uint32_t dst = cur[b] + (uint32_t)r;
+            const int b = stb[i];
+            const uint32_t dst = cur[b] + (uint32_t)(i - lst[b]);
             dk[dst] = stk[i];
             if constexpr (PB != 0) dp[dst] = stp[i];
         }
