@@ -50,6 +50,9 @@ def load(auto_build: bool = True):
     if _lib is not None:
         return _lib
     path = _build.LIB
+    variant = os.environ.get("ZSB_LIB_VARIANT")  # experiments: an in-tree build variant, libzsort_b200_<v>.so
+    if variant:
+        path, auto_build = path[:-3] + f"_{variant}.so", False
     if auto_build and _build.needs_build():
         try:
             _build.build()

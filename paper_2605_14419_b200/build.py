@@ -45,6 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     extra = ["-DZSB_PHASE_PROFILE"] if os.environ.get("ZSB_PHASE_PROFILE") == "1" else []
+    extra += os.environ.get("ZSB_NVCC_EXTRA", "").split()
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", LIB + ".tmp", *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -1299,7 +1299,7 @@ __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned l
 // output store, so src may alias the output (in-place refinement).
 
 constexpr int FIN_INS = 32;         // sub-buckets up to this size are ranked by comparison
-constexpr int FIN_SBITS_MAX = 13;   // <= 8192 sub-buckets (16-bit cursors)
+constexpr int FIN_SBITS_MAX = 14;   // <= 16384 sub-buckets (16-bit cursors)
 constexpr int FIN_BIG_MAX = 512;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
 
 constexpr int FT = 512;         // threads per finish CTA
@@ -1312,15 +1312,15 @@ struct FinItems {
 
 struct FinLayout {
     int cap;
-    size_t off_o, off_pb, off_i, off_cur, off_st, off_bcnt, total;
+    size_t off_o, off_pb, off_i, off_cur, off_bcnt, total;
 };
 
 __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     FinLayout L;
     L.cap = cap;
     size_t o = 0;
-    L.off_o = o;
-    o += (size_t)cap * 8;
+    L.off_o = o;  // placement buffer; first the keys staged in input order (+16 B alignment slack)
+    o += (size_t)cap * 8 + 16;
     L.off_pb = o;  // payload staged in input order by a TMA bulk copy (+16 B alignment slack)
     o += (size_t)cap * pb + (pb ? 16 : 0);
     o = (o + 15) & ~(size_t)15;
@@ -1329,8 +1329,6 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     o = (o + 15) & ~(size_t)15;
     L.off_cur = o;  // S 16-bit counters/cursors, packed two per word
     o += (size_t)(1 << FIN_SBITS_MAX) * 2;
-    L.off_st = o;
-    o += (size_t)((1 << FIN_SBITS_MAX) + 2) * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_bcnt = o;
     o += (size_t)FIN_BIG_MAX * FW * 2 + (1 << FIN_SBITS_MAX) / 8 + 16;
@@ -1339,30 +1337,58 @@ __host__ __device__ inline FinLayout fin_layout(int cap, int pb) {
     return L;
 }
 
-// Stage src[0, m) into shared memory with the same address phase modulo 16,
-// so element i lands at the returned pointer + i: thread 0 issues one TMA
-// bulk copy of the 16-byte-aligned interior (tracked by `bar`), threads 1..
-// load the ragged head and tail.  Readers wait on `bar` and need a barrier
-// after this call for the plain part.
-template <typename T>
-__device__ __forceinline__ const T *stage_range(unsigned char *area, const T *src, int m, uint64_t *bar) {
-    const uintptr_t A = (uintptr_t)src, E = A + (uintptr_t)m * sizeof(T);
+// TMA staging of a contiguous range src[0, m) into shared memory with the
+// same address phase modulo 16, so element i lands at st + i: one bulk copy
+// of the 16-byte-aligned interior plus plain loads of the ragged head
+// [0, h) and tail [t0, m) (a few elements).
+struct StageSpan {
+    uintptr_t a16;    // first aligned byte of the interior
+    uint32_t bytes;   // interior bytes (0: no bulk part)
+    uint32_t phase;   // A & 15
+    int h, t0;
+};
+
+__device__ __forceinline__ StageSpan stage_span(const void *src, int m, int esz) {
+    const uintptr_t A = (uintptr_t)src, E = A + (uintptr_t)m * esz;
     const uintptr_t A16 = (A + 15) & ~(uintptr_t)15, E16 = E & ~(uintptr_t)15;
-    T *st = (T *)(area + (A & 15));
     const bool bulk = E16 > A16;
-    const int h = bulk ? (int)((A16 - A) / sizeof(T)) : m;  // head [0, h)
-    const int t0 = bulk ? (int)((E16 - A) / sizeof(T)) : m;  // tail [t0, m)
+    return StageSpan{A16, bulk ? (uint32_t)(E16 - A16) : 0u, (uint32_t)(A & 15),
+                     bulk ? (int)((A16 - A) / esz) : m, bulk ? (int)((E16 - A) / esz) : m};
+}
+
+// Stage the keys (and payload) of a finish run into shared memory with one
+// mbarrier phase: thread 0 arms it with the total interior bytes and issues
+// the bulk copies; warps 1 and 2 load the ragged ends.  Callers wait on `bar`
+// and then barrier before reading.
+template <typename P, int PB>
+__device__ __forceinline__ void stage_run(unsigned char *karea, const uint64_t *sk, unsigned char *parea, const P *sp,
+                                          int m, uint64_t *bar, const uint64_t *&kst, const P *&pst) {
+    const StageSpan ks = stage_span(sk, m, 8);
+    uint64_t *kd = (uint64_t *)(karea + ks.phase);
+    kst = kd;
+    StageSpan ps{};
+    P *pd = nullptr;
+    if constexpr (PB != 0) {
+        ps = stage_span(sp, m, PB);
+        pd = (P *)(parea + ps.phase);
+        pst = pd;
+    }
     const int tid = threadIdx.x;
     if (tid == 0) {
         fence_proxy_async_smem();
-        mbar_expect_tx(bar, bulk ? (uint32_t)(E16 - A16) : 0u);
-        if (bulk) bulk_g2s((unsigned char *)st + (A16 - A), (const void *)A16, (uint32_t)(E16 - A16), bar);
-    } else if (tid - 1 < h) {
-        st[tid - 1] = src[tid - 1];
-    } else if (tid - 1 - h < m - t0) {
-        st[t0 + tid - 1 - h] = src[t0 + tid - 1 - h];
+        mbar_expect_tx(bar, ks.bytes + ps.bytes);
+        if (ks.bytes) bulk_g2s((unsigned char *)kd + (ks.a16 - (uintptr_t)sk), (const void *)ks.a16, ks.bytes, bar);
+        if (PB != 0 && ps.bytes)
+            bulk_g2s((unsigned char *)pd + (ps.a16 - (uintptr_t)sp), (const void *)ps.a16, ps.bytes, bar);
+    } else if (tid >= 32 && tid < 64) {  // key ends
+        const int q = tid - 32;
+        if (q < ks.h) kd[q] = sk[q];
+        else if (q - ks.h < m - ks.t0) kd[ks.t0 + q - ks.h] = sk[ks.t0 + q - ks.h];
+    } else if (PB != 0 && tid >= 64 && tid < 96) {  // payload ends
+        const int q = tid - 64;
+        if (q < ps.h) pd[q] = sp[q];
+        else if (q - ps.h < m - ps.t0) pd[ps.t0 + q - ps.h] = sp[ps.t0 + q - ps.h];
     }
-    return st;
 }
 
 template <int KK, int PB>
@@ -1381,7 +1407,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     uint64_t *Bo = (uint64_t *)(smem + L.off_o);  // ordered key images, placed
     uint16_t *Ix = (uint16_t *)(smem + L.off_i);  // record index of each placed element
     uint32_t *cw = (uint32_t *)(smem + L.off_cur);  // 16-bit counters, two per word
-    uint16_t *sst = (uint16_t *)(smem + L.off_st);
     uint16_t *bcnt = (uint16_t *)(smem + L.off_bcnt);
     uint32_t *bigmask = (uint32_t *)(smem + L.off_bcnt + FIN_BIG_MAX * FW * 2);
     __shared__ unsigned long long r_min[FW], r_max[FW];
@@ -1398,22 +1423,23 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     P *op = (P *)B.out_p + e.start;
     const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
     const int base = w * 32 * F + lane;
-    // payload: staged in input order by the TMA, gathered by record index at
-    // the store (no registers held through the sort)
+    // keys and payload arrive in input order by TMA bulk copies (the copy
+    // engine keeps far more bytes in flight than per-thread loads); keys are
+    // staged in the placement buffer, which is free until placement, and
+    // moved to registers; the payload stays staged and is gathered by
+    // record index at the store
+    const uint64_t *kin = nullptr;
     const P *pin = nullptr;
-    if constexpr (PB != 0) pin = stage_range<P>(smem + L.off_pb, sp, m, bar);
-    auto pay_wait = [&]() {
-        if constexpr (PB != 0) {
-            mbar_wait(bar, parity);
-            parity ^= 1u;
-        }
-    };
+    stage_run<P, PB>(smem + L.off_o, sk, smem + L.off_pb, sp, m, bar, kin, pin);
+    mbar_wait(bar, parity);
+    parity ^= 1u;
+    __syncthreads();
 
     uint64_t o[F];
 #pragma unroll
     for (int j = 0; j < F; j++) {
         const int i = base + j * 32;
-        o[j] = i < m ? sk[i] : 0ull;
+        o[j] = i < m ? kin[i] : 0ull;
     }
     if (tid == 0) nbig = 0;
     bool anyneg = false;
@@ -1439,11 +1465,12 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     }
     if constexpr (KK == KEY_F64) anyneg = __syncthreads_or(anyneg);
     else __syncthreads();
+    FIN_MARK(1);  // loads landed
     if constexpr (KK == KEY_F64) {
         if (anyneg) {  // -0.0 and +0.0 share an ordered image; remember which records were -0.0
 #pragma unroll
             for (int j = 0; j < F; j++)
-                if (base + j * 32 < m && o[j] == ord_key<KK>(SIGN) && sk[base + j * 32] == SIGN)
+                if (base + j * 32 < m && o[j] == ord_key<KK>(SIGN) && kin[base + j * 32] == SIGN)
                     atomicOr(&negzero[(base + j * 32) >> 5], 1u << lane);
             __syncthreads();
         }
@@ -1461,7 +1488,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         return kb;
     };
     if (omin == omax) {  // all equal: already in stable order
-        pay_wait();
         if (e.src != 2) {
 #pragma unroll
             for (int j = 0; j < F; j++) {
@@ -1476,6 +1502,10 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     }
     int sbits = 5;
     while ((1 << sbits) < m && sbits < FIN_SBITS_MAX) sbits++;
+#ifndef ZSB_FIN_S2
+#define ZSB_FIN_S2 1
+#endif
+    if (ZSB_FIN_S2 && (1 << sbits) < 2 * m && sbits < FIN_SBITS_MAX) sbits++;  // S >= 2m when it fits
     const int S = 1 << sbits;
     const uint64_t range = omax - omin;
     const bool direct = range < (uint64_t)S;  // one key value per digit
@@ -1484,14 +1514,34 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     const int sh = max(0, bitlen64(range) - 32);
     const uint32_t r32 = (uint32_t)(range >> sh);
     const uint32_t M = direct ? 0u : (uint32_t)((((uint64_t)S) << 32) / ((uint64_t)r32 + 1));
+    // float64 keys over a finite range take their digit in value space: the
+    // ordered images are exponentially non-uniform near 0 (a run straddling
+    // 0 would crowd into a few digits).  Rounded subtraction and product by a
+    // positive constant keep the digit monotone in the key.
+    bool vdig = false;
+    double vlo = 0.0, vinv = 0.0;
+    if constexpr (KK == KEY_F64) {
+        const double lo = key_value<KK>(key_from_ord<KK>(omin)), hi = key_value<KK>(key_from_ord<KK>(omax));
+        const double span = __dsub_rn(hi, lo);
+        vinv = (double)S / span;
+#ifndef ZSB_FIN_VDIG
+#define ZSB_FIN_VDIG 1
+#endif
+        vdig = ZSB_FIN_VDIG && isfinite(lo) && isfinite(hi) && span > 0.0 && isfinite(span) && isfinite(vinv) && !direct;
+        vlo = lo;
+    }
     auto digit = [&](uint64_t ov) -> int {
+        if (KK == KEY_F64 && vdig) {
+            const int d = (int)__dmul_rn(__dsub_rn(key_value<KK>(key_from_ord<KK>(ov)), vlo), vinv);
+            return d < S ? d : S - 1;
+        }
         const uint64_t x = ov - omin;
         return direct ? (int)x : (int)__umulhi((uint32_t)(x >> sh), M);
     };
     for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
     for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
     __syncthreads();
-    FIN_MARK(1);
+    FIN_MARK(2);
     // ---- histogram (16-bit counters: no carry, counts <= cap < 2^16)
     uint32_t dpk[(F + 1) / 2];  // digits, two per register
 #pragma unroll
@@ -1502,37 +1552,26 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         if (d != 0xFFFF) atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
     }
     __syncthreads();
-    FIN_MARK(2);
-    // ---- exclusive scan -> sst (starts) and cursors; flag oversized digits.
-    //      Thread t owns digits [t*per, (t+1)*per) (per = S/FT, 0 or a
-    //      multiple of 8 except when S < FT*8); 16-byte vector accesses.
+    FIN_MARK(3);
+    // ---- exclusive scan of the counters in place (they become the cursors;
+    //      after placement cursor d = start of d + 1, so no separate start
+    //      table); flag oversized digits.  Thread t owns digits
+    //      [t*per, (t+1)*per), per = S/FT in {0 (S < FT), 1, 2, 4, 8, 16, 32},
+    //      with 16-byte vector accesses from 8 on.
     {
         uint16_t *c16 = (uint16_t *)cw;
-        const int per = S / FT;  // S >= 32; per in {0 (S<FT), 1, 2, 4, 8, 16}
+        const int per = S / FT;
         const int d0 = per ? tid * per : (tid < S ? tid : S), d1 = per ? d0 + per : (tid < S ? tid + 1 : S);
-        uint16_t v[16];
+        auto sum8 = [](uint4 u) {
+            return (u.x & 0xffffu) + (u.x >> 16) + (u.y & 0xffffu) + (u.y >> 16) + (u.z & 0xffffu) + (u.z >> 16) +
+                   (u.w & 0xffffu) + (u.w >> 16);
+        };
         uint32_t tsum = 0;
         if (per >= 8) {
-#pragma unroll
-            for (int q = 0; q < 2; q++) {
-                if (q * 8 < per) {
-                    const uint4 u = *(const uint4 *)(c16 + d0 + q * 8);
-                    const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                    for (int r = 0; r < 4; r++) {
-                        v[q * 8 + 2 * r] = (uint16_t)(wv[r] & 0xffff);
-                        v[q * 8 + 2 * r + 1] = (uint16_t)(wv[r] >> 16);
-                    }
-                }
-            }
+            for (int q = 0; q < per; q += 8) tsum += sum8(*(const uint4 *)(c16 + d0 + q));
         } else {
-#pragma unroll
-            for (int q = 0; q < 16; q++)
-                if (q < d1 - d0) v[q] = c16[d0 + q];
+            for (int d = d0; d < d1; d++) tsum += c16[d];
         }
-#pragma unroll
-        for (int q = 0; q < 16; q++)
-            if (q < d1 - d0) tsum += v[q];
         uint32_t x = tsum;
 #pragma unroll
         for (int q = 1; q < 32; q <<= 1) {
@@ -1543,45 +1582,36 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         __syncthreads();
         uint32_t run = x - tsum;
         for (int q = 0; q < w; q++) run += wsum[q];
-        uint16_t e[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) {
-            if (q < d1 - d0) {
-                e[q] = (uint16_t)run;
-                if (v[q] > (uint32_t)fin_ins) {
-                    const int d = d0 + q;
-                    const int bi = atomicAdd(&nbig, 1);
-                    if (bi < FIN_BIG_MAX) bslot[bi] = (uint16_t)d;
-                    atomicOr(&bigmask[d >> 5], 1u << (d & 31));
-                }
-                run += v[q];
+        auto excl = [&](uint32_t v, int d) -> uint32_t {  // start of digit d (count v); flags oversized
+            const uint32_t st = run;
+            if (v > (uint32_t)fin_ins) {
+                const int bi = atomicAdd(&nbig, 1);
+                if (bi < FIN_BIG_MAX) bslot[bi] = (uint16_t)d;
+                atomicOr(&bigmask[d >> 5], 1u << (d & 31));
             }
-        }
+            run += v;
+            return st;
+        };
         if (per >= 8) {
+            for (int q = 0; q < per; q += 8) {
+                const uint4 u = *(const uint4 *)(c16 + d0 + q);
+                const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+                uint32_t ov[4];
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-                if (q * 8 < per) {
-                    const uint4 u = make_uint4(e[q * 8] | ((uint32_t)e[q * 8 + 1] << 16),
-                                               e[q * 8 + 2] | ((uint32_t)e[q * 8 + 3] << 16),
-                                               e[q * 8 + 4] | ((uint32_t)e[q * 8 + 5] << 16),
-                                               e[q * 8 + 6] | ((uint32_t)e[q * 8 + 7] << 16));
-                    *(uint4 *)(c16 + d0 + q * 8) = u;
-                    *(uint4 *)(sst + d0 + q * 8) = u;
+                for (int r = 0; r < 4; r++) {
+                    const uint32_t lo = excl(wv[r] & 0xffffu, d0 + q + 2 * r);
+                    const uint32_t hi = excl(wv[r] >> 16, d0 + q + 2 * r + 1);
+                    ov[r] = lo | (hi << 16);
                 }
+                *(uint4 *)(c16 + d0 + q) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
             }
         } else {
-#pragma unroll
-            for (int q = 0; q < 16; q++)
-                if (q < d1 - d0) {
-                    c16[d0 + q] = e[q];
-                    sst[d0 + q] = e[q];
-                }
+            for (int d = d0; d < d1; d++) c16[d] = (uint16_t)excl(c16[d], d);
         }
-        if (tid == FT - 1) sst[S] = (uint16_t)m;
     }
     __syncthreads();
     const int nb = nbig;  // <= m / (fin_ins + 1) <= FIN_BIG_MAX
-    FIN_MARK(3);
+    FIN_MARK(4);
     // ---- place (atomic cursors; oversized digits go through the stable path)
 #pragma unroll
     for (int j = 0; j < F; j++) {
@@ -1631,12 +1661,14 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         }
         __syncthreads();
         for (int q = tid; q < nb; q += FT) {  // exclusive prefix over warps from the digit's start
-            uint32_t run = sst[bslot[q]];
+            uint16_t *cur_d = (uint16_t *)cw + bslot[q];
+            uint32_t run = *cur_d;  // not advanced by the atomic placement: still the start
             for (int ww = 0; ww < FW; ww++) {
                 const uint32_t c = bcnt[q * FW + ww];
                 bcnt[q * FW + ww] = (uint16_t)run;
                 run += c;
             }
+            *cur_d = (uint16_t)run;  // end of the digit, like every other cursor
         }
         __syncthreads();
 #pragma unroll
@@ -1658,16 +1690,15 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             }
         }
     }
-    pay_wait();
     __syncthreads();
-    FIN_MARK(4);
+    FIN_MARK(5);
     // ---- rank inside each sub-bucket by (key, record index) and store to
     //      the final position; ties keep input order (stable)
     for (int i = tid; i < m; i += FT) {
         const uint64_t ov = Bo[i];
         const int idx = Ix[i];
         const int d = digit(ov);
-        const int a = sst[d], z = sst[d + 1];
+        const int a = d ? (int)((const uint16_t *)cw)[d - 1] : 0, z = ((const uint16_t *)cw)[d];
         const int c = z - a;
         int rank = i - a;
         if (c <= fin_ins) {
@@ -1689,7 +1720,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         ok[a + rank] = key_bits(ov, idx);
         if constexpr (PB != 0) op[a + rank] = pin[idx];
     }
-    FIN_MARK(5);
     FIN_MARK(6);
 #undef FIN_MARK
 }
@@ -1702,10 +1732,10 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
                                                   Entry *refine, unsigned long long *refine_count, int fin_ins,
                                                   long long *prof, unsigned long long *ticket) {
     __shared__ long long next;
-    __shared__ uint64_t bar;  // payload staging (TMA bulk copy) completion
+    __shared__ uint64_t bar;  // run staging (TMA bulk copies) completion
     uint32_t parity = 0;
     const int64_t ne = count ? (int64_t)*count : count_const;
-    if (PB != 0 && threadIdx.x == 0) mbar_init(&bar, 1);
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     if (!ticket) {  // one run per CTA (grid = exact count)
         if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,

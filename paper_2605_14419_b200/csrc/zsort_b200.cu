@@ -354,7 +354,7 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
 long long *g_fin_prof = nullptr;
 int64_t g_fin_prof_n = 0;
 long long *fin_prof(int64_t n) {
-    if (!env_int("ZSB_FIN_PROFILE", 0) || n < g_fin_prof_n) return nullptr;
+    if (!env_int("ZSB_FIN_PROFILE", 0) || n <= g_fin_prof_n) return nullptr;  // first launch of the largest size
     if (g_fin_prof) cudaFree(g_fin_prof);
     cudaMalloc(&g_fin_prof, (size_t)n * 8 * 8);
     cudaMemset(g_fin_prof, 0, (size_t)n * 8 * 8);
@@ -374,8 +374,8 @@ void fin_prof_dump() {
         cnt++;
         for (int q = 1; q <= 6; q++) acc[q] += (double)(t[q] - t[q - 1]);
     }
-    fprintf(stderr, "[zsb] finish phases over %lld CTAs (cycles): load+minmax %.0f hist %.0f scan %.0f place %.0f "
-                    "order %.0f store %.0f\n", (long long)cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+    fprintf(stderr, "[zsb] finish phases over %lld CTAs (cycles): load %.0f minmax+params %.0f hist %.0f scan %.0f "
+                    "place %.0f rank+store %.0f\n", (long long)cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
             acc[5] / cnt, acc[6] / cnt);
     cudaFree(g_fin_prof);
     g_fin_prof = nullptr;
