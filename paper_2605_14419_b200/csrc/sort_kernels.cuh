@@ -553,11 +553,11 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
     L.off_cur = o;
     o += (size_t)k * 4;
     o = (o + 15) & ~(size_t)15;
-    L.off_cnt = o;
-    o += (size_t)k * sw * 2;
+    L.off_cnt = o;  // two counter sets (consecutive rounds alternate)
+    o += (size_t)2 * k * sw * 2;
     o = (o + 15) & ~(size_t)15;
-    L.off_lst = o;
-    o += (size_t)(k + 1) * 2;
+    L.off_lst = o;  // two run-start tables
+    o += (size_t)2 * (k + 2) * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_k = o;
     o += (size_t)round * 8;
@@ -570,57 +570,6 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
     L.off_cdf = o;  // the CDF table (level-1 equalisation only) follows the layout
     L.total = o;
     return L;
-}
-
-// Exclusive scan, in (digit, warp) order, of per-(digit, warp) u16 counters
-// laid out [digit][SW] (SW/8 uint4 per digit).  Thread t owns digits
-// [t*per, (t+1)*per): a thread-local pass over its uint4s, one block scan
-// of the thread totals, and a write-back pass.  Also writes the digit
-// starts to dstart[0..ndig] (dstart[ndig] = total).  Ends with a barrier.
-template <int SW>
-__device__ __forceinline__ void scan_dw(uint16_t *cnt, int ndig, uint16_t *dstart, uint32_t *wsum) {
-    constexpr int T = SW * 32, V = SW / 8;
-    const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-    const int per = (ndig + T - 1) / T;
-    const int d0 = min(ndig, tid * per), d1 = min(ndig, d0 + per);
-    uint4 *c4 = (uint4 *)cnt;
-    uint32_t tsum = 0;
-    for (int d = d0; d < d1; d++) {
-#pragma unroll
-        for (int v = 0; v < V; v++) {
-            const uint4 x = c4[d * V + v];
-            tsum += (x.x & 0xffff) + (x.x >> 16) + (x.y & 0xffff) + (x.y >> 16) + (x.z & 0xffff) + (x.z >> 16) +
-                    (x.w & 0xffff) + (x.w >> 16);
-        }
-    }
-    uint32_t x = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    uint32_t run = x - tsum;
-    for (int q = 0; q < w; q++) run += wsum[q];
-    for (int d = d0; d < d1; d++) {
-        dstart[d] = (uint16_t)run;
-#pragma unroll
-        for (int v = 0; v < V; v++) {
-            const uint4 xv = c4[d * V + v];
-            uint32_t h[8] = {xv.x & 0xffff, xv.x >> 16, xv.y & 0xffff, xv.y >> 16,
-                             xv.z & 0xffff, xv.z >> 16, xv.w & 0xffff, xv.w >> 16};
-            uint32_t e[8];
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                e[q] = run;
-                run += h[q];
-            }
-            c4[d * V + v] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
-        }
-    }
-    if (tid == T - 1) dstart[ndig] = (uint16_t)run;
-    __syncthreads();
 }
 
 // Exclusive scan in (digit, warp) order of per-(warp, digit) u16 counters laid
@@ -705,9 +654,10 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     }
     const int k = p.k;
     const ScatLayout L = scat_layout(k, PB, SW);
+    const int NC = k * SW;
     uint32_t *cur = (uint32_t *)(smem + L.off_cur);
-    uint16_t *cnt = (uint16_t *)(smem + L.off_cnt);
-    uint16_t *lst = (uint16_t *)(smem + L.off_lst);
+    uint16_t *cnt2 = (uint16_t *)(smem + L.off_cnt);  // [2][SW][k]
+    uint16_t *lst2 = (uint16_t *)(smem + L.off_lst);  // [2][k + 2]
     uint64_t *stk = (uint64_t *)(smem + L.off_k);
     P *stp = (P *)(smem + L.off_p);
     uint16_t *stb = (uint16_t *)(smem + L.off_b);
@@ -718,16 +668,18 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     P *dp = (P *)(dst_sel == 1 ? B.tmp_p : B.out_p);
     const uint32_t *col = mat + p.mat_base + ti;
     const uint32_t adj = (uint32_t)(p.start - p.scan_base);
-    const int NC = k * SW;
     for (int b = threadIdx.x; b < k; b += ST) cur[b] = col[(int64_t)b * p.ntiles] + adj;
-    for (int q = threadIdx.x; q < NC; q += ST) cnt[q] = 0;
+    for (int q = threadIdx.x; q < 2 * NC; q += ST) cnt2[q] = 0;
     __syncthreads();
 
     const int w = threadIdx.x >> 5, lane = lane_id();
-    // Software pipeline: the keys of round r+1 are loaded right after round
-    // r's placement (key[] is free then) and land during its write phase;
-    // payload loads are issued at the start of a round and consumed only at
-    // placement, behind the bucket / count / scan phases.
+    const unsigned lt = lanemask_lt();
+    // Pipeline across rounds.  Round r's staged records are written to HBM
+    // while round r+1 computes its buckets and counts (phase A), so the store
+    // traffic overlaps the arithmetic; counters and run-start tables
+    // alternate between two sets so no barrier separates the two.  Keys of
+    // round r+1 are loaded during round r's placement; payloads at the start
+    // of their round, consumed at placement.
     const int base = w * 32 * ITEMS + lane;
     uint64_t key[ITEMS];
     {
@@ -735,55 +687,61 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nv0 ? __ldcs(sk + t0 + base + j * 32) : 0ull;
     }
+    int rb = 0, prev_nvalid = 0;  // counter/run-start set of this round; records staged by the previous round
     for (int64_t r0 = t0; r0 < t1; r0 += ROUND) {
         SCAT_MARK(5);
         const int nvalid = (int)min((int64_t)ROUND, t1 - r0);
+        uint16_t *cnt = cnt2 + rb * NC;
+        uint16_t *lst = lst2 + rb * (k + 2);
+        const uint16_t *lstp = lst2 + (rb ^ 1) * (k + 2);
         P pay[ITEMS];
-        int bk[ITEMS];
         if constexpr (PB != 0) {
 #pragma unroll
             for (int j = 0; j < ITEMS; j++) pay[j] = base + j * 32 < nvalid ? __ldcs(sp + r0 + base + j * 32) : (P)0;
         }
-#pragma unroll
-        for (int j = 0; j < ITEMS; j++)
-            bk[j] = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
-        SCAT_MARK(0);  // loads + bucket ids
-        // count: one shared atomic per item on its per-(warp, bucket) u16
-        // counter; the returned count is the item's rank among its warp's
-        // items of that bucket.  A warp's shared-memory operations execute in
-        // program order, so ranks follow j (input order); only lanes of one
-        // instruction that share a bucket (a tie group) may be ranked out of
-        // lane order.  Re-reading the counter right after the atomic exposes
-        // them (a member that is not its group's last sees the counter move by
-        // more than its own increment); only then does the warp pay for
-        // __match_any_sync, and the group is re-ranked in lane order from its
-        // end value.  Random keys tie in ~40% of instructions (k = 1024),
-        // sorted runs in all of them but with few distinct buckets, where the
-        // match is cheap.
+        // phase A: bucket + rank of item j (one shared atomic on its
+        // per-(warp, bucket) u16 counter: the returned count is its rank among
+        // its warp's items of that bucket; a warp's shared-memory operations
+        // execute in program order, so ranks follow j; lanes of one
+        // instruction that share a bucket -- a tie group -- are exposed by
+        // re-reading the counter and re-ranked in lane order with a match,
+        // paid only by warp instructions that have one), interleaved with the
+        // coalesced write of staged slot tid + j*ST of the previous round.
         uint32_t pk[ITEMS];  // bucket | rank << 16
-        const unsigned lt = lanemask_lt();
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
+            const int bkj = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
             uint32_t old = 0, after = 0;
-            const int q = w * k + (bk[j] < 0 ? 0 : bk[j]);
+            const int q = w * k + (bkj < 0 ? 0 : bkj);
             const uint32_t sh = 16 * (q & 1);
             uint32_t *word = (uint32_t *)cnt + (q >> 1);
-            if (bk[j] >= 0) {
+            if (bkj >= 0) {
                 old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
                 after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
             }
-            const bool tie = bk[j] >= 0 && after != old + 1u;
+            const bool tie = bkj >= 0 && after != old + 1u;
             if (__any_sync(0xffffffffu, tie)) {
-                const unsigned m = __match_any_sync(0xffffffffu, bk[j]);
-                if (bk[j] >= 0 && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
+                const unsigned m = __match_any_sync(0xffffffffu, bkj);
+                if (bkj >= 0 && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
             }
-            pk[j] = bk[j] >= 0 ? (uint32_t)bk[j] | (old << 16) : 0xffffffffu;
+            pk[j] = bkj >= 0 ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
+            const int i = threadIdx.x + j * ST;
+            if (i < prev_nvalid) {
+                const int b = stb[i];
+                const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
+                dk[dst] = stk[i];
+                if constexpr (PB != 0) dp[dst] = stp[i];
+            }
         }
         __syncthreads();
-        SCAT_MARK(1);  // counting
+        SCAT_MARK(1);  // buckets + counting + previous round's writes
+        // phase B: cursors advance past the previous round's runs; scan
+        if (prev_nvalid)
+            for (int b = threadIdx.x; b < k; b += ST) cur[b] += (uint32_t)(lstp[b + 1] - lstp[b]);
         scan_wd<SW>(cnt, k, lst, wtot);
         SCAT_MARK(2);  // scan
-        // place: slot = (warp, bucket) base + rank
+        // phase C: place (slot = (warp, bucket) base + rank); clear the other
+        // counter set for the next round; load the next round's keys
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
             if (pk[j] != 0xffffffffu) {
@@ -794,27 +752,29 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
                 stb[pos] = (uint16_t)b;
             }
         }
-        __syncthreads();
-        SCAT_MARK(3);  // placement
-        {  // prefetch the next round's keys
+        {
+            uint16_t *cn = cnt2 + (rb ^ 1) * NC;
+            for (int q = threadIdx.x; q < NC / 2; q += ST) ((uint32_t *)cn)[q] = 0u;
             const int64_t rn = r0 + ROUND;
             const int nvn = rn < t1 ? (int)min((int64_t)ROUND, t1 - rn) : 0;
 #pragma unroll
             for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nvn ? __ldcs(sk + rn + base + j * 32) : 0ull;
         }
-        // coalesced run writes
-        for (int i = threadIdx.x; i < nvalid; i += ST) {
+        __syncthreads();
+        SCAT_MARK(3);  // placement
+        prev_nvalid = nvalid;
+        rb ^= 1;
+    }
+    {  // epilogue: write the last round
+        const uint16_t *lstp = lst2 + (rb ^ 1) * (k + 2);
+        for (int i = threadIdx.x; i < prev_nvalid; i += ST) {
             const int b = stb[i];
-            const uint32_t dst = cur[b] + (uint32_t)(i - lst[b]);
+            const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
             dk[dst] = stk[i];
             if constexpr (PB != 0) dp[dst] = stp[i];
         }
-        for (int q = threadIdx.x; q < NC; q += ST) cnt[q] = 0;
-        __syncthreads();
-        for (int b = threadIdx.x; b < k; b += ST) cur[b] += (uint32_t)(lst[b + 1] - lst[b]);
-        __syncthreads();
-        SCAT_MARK(4);  // writes + cursor update
     }
+    SCAT_MARK(4);
 #ifdef ZSB_PHASE_PROFILE
     if (prof && threadIdx.x == 0)
         for (int q = 0; q < 6; q++) prof[(int64_t)blockIdx.x * 8 + q] = acc_ph[q];
