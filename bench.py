@@ -236,8 +236,6 @@ def main():
         while time.perf_counter() < t_end:
             sort_once()
         torch.cuda.synchronize()
-        L.zsb_timing_read(ms_phase, launches, 8, 1)
-        L.zsb_timing_enable(1)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -253,6 +251,14 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+    # per-phase breakdown (CUDA events around each launch group) in a separate
+    # pass of the same steps, so the events do not perturb the timed steps
+    L.zsb_timing_read(ms_phase, launches, 8, 1)
+    L.zsb_timing_enable(1)
+    for _ in range(args.steps):
+        flush.zero_()
+        sort_once()
+    torch.cuda.synchronize()
     L.zsb_timing_enable(0)
     L.zsb_timing_read(ms_phase, launches, 8, 1)
     total_ms = sum(step_ms)

@@ -106,6 +106,10 @@ enum Ctrl {
     C_FTICK1 = 17,
     C_SAMP_TICKET = 18,  // sampled level-1 kernels
     C_SAMPLE_OK = 19,    // 1: level 1 mapped from the sample (exact K1 skipped)
+    C_NREF2 = 20,        // refine lists of odd levels (C_NREF0/1: even levels)
+    C_NREF3 = 21,
+    C_FTICK2 = 22,
+    C_FTICK3 = 23,
     C_SLOTS = 24
 };
 

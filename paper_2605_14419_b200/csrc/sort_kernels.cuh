@@ -1694,7 +1694,7 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
     __shared__ long long next;
     __shared__ uint64_t bar;  // run staging (TMA bulk copies) completion
     uint32_t parity = 0;
-    const int64_t ne = count ? (int64_t)*count : count_const;
+    const int64_t ne = count ? min((int64_t)*count, count_const) : count_const;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     if (!ticket) {  // one run per CTA (grid = exact count)

@@ -158,8 +158,8 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
 }
 
 struct Layout {
-    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, wfirst, bstart, entries, refine0, refine1, parts,
-        ctrl, dbg, fine, lut, total;
+    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, wfirst, bstart, entries, refine[4], parts, ctrl,
+        dbg, fine, lut, total;
     int64_t mat_cap, seg_cap, ent_cap, status_cap, slot_cap, ref_cap;
 };
 
@@ -199,10 +199,10 @@ Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
     o = align_up(o + (size_t)L.slot_cap * 8);
     L.entries = o;
     o = align_up(o + (size_t)L.ent_cap * sizeof(Entry));
-    L.refine0 = o;
-    o = align_up(o + (size_t)L.ref_cap * sizeof(Entry));
-    L.refine1 = o;
-    o = align_up(o + (size_t)L.ref_cap * sizeof(Entry));
+    for (int q = 0; q < 4; q++) {
+        L.refine[q] = o;
+        o = align_up(o + (size_t)L.ref_cap * sizeof(Entry));
+    }
     L.parts = o;
     o = align_up(o + (size_t)num_sms() * MOM_GRID_PER_SM * sizeof(MomPartial));
     L.ctrl = o;
@@ -302,8 +302,8 @@ void scat_prof_dump() {
     double acc[6] = {0};
     for (int64_t b = 0; b < g_scat_prof_n; b++)
         for (int q = 0; q < 6; q++) acc[q] += (double)h[(size_t)b * 8 + q];
-    fprintf(stderr, "[zsb] scatter phases per CTA (cycles, summed over rounds): loads+buckets %.0f match+count %.0f "
-                    "scan %.0f place %.0f write %.0f loop %.0f\n", acc[0] / g_scat_prof_n, acc[1] / g_scat_prof_n,
+    fprintf(stderr, "[zsb] scatter phases per CTA (cycles, summed over rounds): - %.0f buckets+rank+prev-writes %.0f "
+                    "scan %.0f place+next-keys %.0f last-writes %.0f loop %.0f\n", acc[0] / g_scat_prof_n, acc[1] / g_scat_prof_n,
             acc[2] / g_scat_prof_n, acc[3] / g_scat_prof_n, acc[4] / g_scat_prof_n, acc[5] / g_scat_prof_n);
     cudaFree(g_scat_prof);
     g_scat_prof = nullptr;
@@ -382,27 +382,52 @@ void fin_prof_dump() {
     g_fin_prof_n = 0;
 }
 
-// Persistent finish over `list`: count from device memory (count_dev) or a
-// host constant; records refine runs into list `ref_out` (0/1).
+// Refine lists: two per level parity (a level's finish writes list 2*par,
+// its refine pass list 2*par + 1), so a level's leftovers survive the next
+// level's finish, which is enqueued before the host has read them.
+constexpr int REF_SLOT[4] = {C_NREF0, C_NREF1, C_NREF2, C_NREF3};
+constexpr int TICK_SLOT[4] = {C_FTICK0, C_FTICK1, C_FTICK2, C_FTICK3};
+
+// Finish over `list`: count from device memory (count_dev, clamped to
+// count_const; persistent CTAs with a work ticket) or the host constant
+// count_const (one run per CTA); refine runs go to refine list `ref_out`.
 template <int KK, int PB>
 int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev, int64_t count_const,
                   int64_t count_bound, int ref_out, int tick) {
     if (count_bound <= 0) return ZSB_OK;
     FinLayout FL = fin_layout((int)c.P.cap, PB);
     smem_optin(k_finish<KK, PB>, FL.total);
-    Entry *refine = (Entry *)(c.ws + (ref_out ? c.L.refine1 : c.L.refine0));
+    Entry *refine = (Entry *)(c.ws + c.L.refine[ref_out]);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
-    // exact host-known count: one run per CTA; device-side count: persistent CTAs
     const int64_t grid = count_dev ? std::min<int64_t>(count_bound, (int64_t)num_sms()) : count_bound;
     {
         PhaseScope ph(PH_FINISH, c.st);
         k_finish<KK, PB><<<(unsigned)grid, FT, FL.total, c.st>>>(c.B, list, count_dev, count_const, (int)c.P.cap, refine,
-                                                                ctrl + (ref_out ? C_NREF1 : C_NREF0),
+                                                                ctrl + REF_SLOT[ref_out],
                                                                 env_int("ZSB_FIN_INS", FIN_INS),
                                                                 fin_prof(count_bound),
-                                                                count_dev ? ctrl + C_FTICK0 + tick : nullptr);
+                                                                count_dev ? ctrl + TICK_SLOT[tick] : nullptr);
     }
     ZSB_LAUNCH("k_finish");
+    return ZSB_OK;
+}
+
+// Pinned host mirror of the control block and the level event (per host thread).
+struct HostSync {
+    unsigned long long *ctrl = nullptr;
+    cudaEvent_t ev = nullptr;
+    int dev = -1;
+};
+thread_local HostSync g_hs;
+
+int host_sync_init() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_hs.ctrl && g_hs.dev == dev) return ZSB_OK;
+    if (!g_hs.ctrl) ZSB_CUDA(cudaHostAlloc((void **)&g_hs.ctrl, C_SLOTS * 8, cudaHostAllocDefault));
+    if (g_hs.ev) cudaEventDestroy(g_hs.ev);
+    ZSB_CUDA(cudaEventCreateWithFlags(&g_hs.ev, cudaEventDisableTiming));
+    g_hs.dev = dev;
     return ZSB_OK;
 }
 
@@ -417,39 +442,52 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int64_t *wfirst = (int64_t *)(c.ws + c.L.wfirst);
     int64_t *bstart = (int64_t *)(c.ws + c.L.bstart);
     Entry *entries = (Entry *)(c.ws + c.L.entries);
-    Entry *refine[2] = {(Entry *)(c.ws + c.L.refine0), (Entry *)(c.ws + c.L.refine1)};
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     int64_t stats[ZSB_STAT_SLOTS] = {0, 0, 0, 0, 0};
-    unsigned long long h_ctrl[C_SLOTS];
+    if (int rc = host_sync_init()) return rc;
+    unsigned long long *hc = g_hs.ctrl;  // pinned: the copies below are truly asynchronous
     ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
-
-    // Finish the runs listed in `list` (count on device) and their refine
-    // runs once, without a host round trip; returns after enqueueing.
-    // Refine runs of the refine pass land in list 1 (count C_NREF1).
-    auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
-                              int64_t bound) -> int {
-        ZSB_CUDA(cudaMemsetAsync(ctrl + C_NREF0, 0, 32, c.st));  // C_NREF0, C_NREF1, C_FTICK0, C_FTICK1
-        int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 0, 0);
-        if (rc) return rc;
-        return launch_finish<KK, PB>(c, refine[0], ctrl + C_NREF0, 0, std::min<int64_t>(bound, c.L.ref_cap), 1, 1);
+    auto full_sync = [&]() -> int {  // control block -> host, wait for everything enqueued
+        ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, c.st));
+        ZSB_CUDA(cudaStreamSynchronize(c.st));
+        timing_collect();
+        return ZSB_OK;
     };
-    // After a sync: drain refine runs of refine runs (rare), ping-ponging lists.
-    auto drain_refine = [&](int64_t pending) -> int {
-        int src = 1;
+
+    // Finish the runs of `list` and, right behind, their refine runs (one
+    // pass, count on the device) without a host round trip; parity `par`
+    // selects the refine lists.
+    auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
+                              int64_t bound, int par) -> int {
+        ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[2 * par], 0, 32, c.st));  // two counts, two tickets
+        int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par);
+        if (rc) return rc;
+        return launch_finish<KK, PB>(c, (const Entry *)(c.ws + c.L.refine[2 * par]), ctrl + REF_SLOT[2 * par],
+                                     c.L.ref_cap, std::min<int64_t>(bound, c.L.ref_cap), 2 * par + 1, 2 * par + 1);
+    };
+    // Refine runs of refine runs (rare): finished from list 2*par + 1 with
+    // host round trips, ping-ponging inside the parity's pair of lists.
+    auto drain_refine = [&](int par, int64_t pending) -> int {
+        int src = 2 * par + 1;
         while (pending > 0) {
             if (pending > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-            ZSB_CUDA(cudaMemsetAsync(ctrl + (src ? C_NREF0 : C_NREF1), 0, 8, c.st));
-            ZSB_CUDA(cudaMemsetAsync(ctrl + C_FTICK0, 0, 8, c.st));
-            int rc = launch_finish<KK, PB>(c, refine[src], nullptr, pending, pending, 1 - src, 0);
+            const int dst = src ^ 1;
+            ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[dst], 0, 8, c.st));
+            int rc = launch_finish<KK, PB>(c, (const Entry *)(c.ws + c.L.refine[src]), nullptr, pending, pending, dst, 0);
             if (rc) return rc;
             stats[ZSB_STAT_INSERTION] += pending;
-            ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
-            ZSB_CUDA(cudaStreamSynchronize(c.st));
-            timing_collect();
-            src = 1 - src;
-            pending = (int64_t)h_ctrl[src ? C_NREF1 : C_NREF0];
+            if ((rc = full_sync())) return rc;
+            src = dst;
+            pending = (int64_t)hc[REF_SLOT[src]];
         }
         return ZSB_OK;
+    };
+    // Counts of a level's finish passes (read after they completed).
+    auto settle_level = [&](int par) -> int {
+        const int64_t n0 = (int64_t)hc[REF_SLOT[2 * par]], n1 = (int64_t)hc[REF_SLOT[2 * par + 1]];
+        if (n0 > c.L.ref_cap || n1 > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
+        stats[ZSB_STAT_INSERTION] += n0;
+        return drain_refine(par, n1);
     };
 
     if (n <= c.P.cap) {  // one shared-memory finish (core.py:369-374; threshold widened to the smem capacity)
@@ -458,14 +496,10 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             k_single_entry<<<1, 1, 0, c.st>>>(entries, n);
         }
         ZSB_LAUNCH("k_single_entry");
-        int rc = enqueue_finish(entries, nullptr, 1, 1);
-        if (rc) return rc;
-        ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
-        ZSB_CUDA(cudaStreamSynchronize(c.st));
-        timing_collect();
-        stats[ZSB_STAT_INSERTION] = 1 + (int64_t)h_ctrl[C_NREF0];
-        rc = drain_refine((int64_t)h_ctrl[C_NREF1]);
-        if (rc) return rc;
+        int rc = enqueue_finish(entries, nullptr, 1, 1, 0);
+        if (rc || (rc = full_sync())) return rc;
+        stats[ZSB_STAT_INSERTION] = 1;
+        if ((rc = settle_level(0))) return rc;
         if (h_stats) memcpy(h_stats, stats, sizeof(stats));
         return ZSB_OK;
     }
@@ -515,7 +549,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int nseg = 1;
     int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
     int kmax = (int)c.P.k;
-    int level = 1;
+    int level = 1, par = 0;
     while (true) {
         if (level > 1) {
             {
@@ -540,45 +574,41 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                                          (int32_t)c.P.half, KMAX_CHILD, MIN_TILE);
         }
         ZSB_LAUNCH("k_bstart/k_windows/k_plan");
-        ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
-        ZSB_CUDA(cudaStreamSynchronize(c.st));
-        timing_collect();
-        if (h_ctrl[C_STATUS] == 3) return fail(ZSB_ERR_NAN, "NaN keys have no order");
-        const int64_t nentry = (int64_t)h_ctrl[C_NENTRY];
-        if (nentry > c.L.ent_cap) return fail(ZSB_ERR_WORKSPACE, "finish list overflow");
-        if (level > 1) {  // refine runs of the previous level's finish, and of their refinement
-            if ((int64_t)h_ctrl[C_NREF0] > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-            stats[ZSB_STAT_INSERTION] += (int64_t)h_ctrl[C_NREF0];
-            rc = drain_refine((int64_t)h_ctrl[C_NREF1]);
-            if (rc) return rc;
-        }
-        // this level's finish runs (one per CTA) and their refine runs (persistent,
-        // count on device), enqueued back to back; the next level starts right after
-        rc = enqueue_finish(entries, nullptr, nentry, nentry);
+        // The host needs this level's outcome (children, sizes of the next
+        // level); the finish of this level does not: it is enqueued before the
+        // host waits (count on the device), so the GPU goes straight on.
+        ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, c.st));
+        ZSB_CUDA(cudaEventRecord(g_hs.ev, c.st));
+        rc = enqueue_finish(entries, ctrl + C_NENTRY, c.L.ent_cap, c.L.ent_cap, par);
         if (rc) return rc;
-        if (env_int("ZSB_DEBUG", 0))
-            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %llu entries %lld fallbacks %llu\n",
-                    level, nseg, (long long)tiles, kmax, h_ctrl[C_NCHILD], (long long)nentry,
-                    h_ctrl[C_ST_FALLBACKS]);
+        ZSB_CUDA(cudaEventSynchronize(g_hs.ev));
+        if (hc[C_STATUS] == 3) {
+            cudaStreamSynchronize(c.st);
+            return fail(ZSB_ERR_NAN, "NaN keys have no order");
+        }
+        const int64_t nentry = (int64_t)hc[C_NENTRY];
+        if (nentry > c.L.ent_cap) {
+            cudaStreamSynchronize(c.st);
+            return fail(ZSB_ERR_WORKSPACE, "finish list overflow");
+        }
         stats[ZSB_STAT_INSERTION] += nentry;
-        int64_t nchild = (int64_t)h_ctrl[C_NCHILD];
+        const int64_t nchild = (int64_t)hc[C_NCHILD];
+        if (env_int("ZSB_DEBUG", 0))
+            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %lld entries %lld fallbacks %llu\n",
+                    level, nseg, (long long)tiles, kmax, (long long)nchild, (long long)nentry, hc[C_ST_FALLBACKS]);
+        if (level > 1 && (rc = settle_level(par ^ 1))) return rc;  // the previous level's passes are done
         if (nchild == 0) {
-            ZSB_CUDA(cudaMemcpyAsync(h_ctrl, ctrl, sizeof(h_ctrl), cudaMemcpyDeviceToHost, c.st));
-            ZSB_CUDA(cudaStreamSynchronize(c.st));
-            timing_collect();
-            if ((int64_t)h_ctrl[C_NREF0] > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-            stats[ZSB_STAT_INSERTION] += (int64_t)h_ctrl[C_NREF0];
-            rc = drain_refine((int64_t)h_ctrl[C_NREF1]);
-            if (rc) return rc;
+            if ((rc = full_sync()) || (rc = settle_level(par))) return rc;
             break;
         }
         if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
         nseg = (int)nchild;
-        tiles = (int64_t)h_ctrl[C_TILES_NEXT];
-        mat_entries = (int64_t)h_ctrl[C_MAT_NEXT];
-        kmax = (int)h_ctrl[C_KMAX_NEXT];
-        total_slots = (int64_t)h_ctrl[C_NEXT_BIG];
-        total_windows = (int64_t)h_ctrl[C_WIN_NEXT];
+        tiles = (int64_t)hc[C_TILES_NEXT];
+        mat_entries = (int64_t)hc[C_MAT_NEXT];
+        kmax = (int)hc[C_KMAX_NEXT];
+        total_slots = (int64_t)hc[C_NEXT_BIG];
+        total_windows = (int64_t)hc[C_WIN_NEXT];
+        par ^= 1;
         if (mat_entries > c.L.mat_cap) return fail(ZSB_ERR_WORKSPACE, "count matrix overflow");
         if (total_slots > c.L.slot_cap) return fail(ZSB_ERR_WORKSPACE, "bucket slot overflow");
         std::swap(seg_cur, seg_next);
@@ -589,9 +619,9 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         fin_prof_dump();
         scat_prof_dump();
     }
-    stats[ZSB_STAT_MAX_DEPTH] = (int64_t)h_ctrl[C_ST_MAXDEPTH];
-    stats[ZSB_STAT_FALLBACKS] = (int64_t)h_ctrl[C_ST_FALLBACKS];
-    stats[ZSB_STAT_SCATTERS] = (int64_t)h_ctrl[C_ST_SCATTERS];
+    stats[ZSB_STAT_MAX_DEPTH] = (int64_t)hc[C_ST_MAXDEPTH];
+    stats[ZSB_STAT_FALLBACKS] = (int64_t)hc[C_ST_FALLBACKS];
+    stats[ZSB_STAT_SCATTERS] = (int64_t)hc[C_ST_SCATTERS];
     if (h_stats) memcpy(h_stats, stats, sizeof(stats));
     return ZSB_OK;
 }
