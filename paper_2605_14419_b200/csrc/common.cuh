@@ -197,24 +197,17 @@ __device__ __forceinline__ int zc_bin(float h, int kf) {
 // units, cdf[0] = 0, cdf[kf] = k).  Clamping each bin to [floor(cdf[s]),
 // floor(cdf[s+1])] keeps the map monotone in the key under any rounding.
 __device__ __forceinline__ int32_t bucket_cdf(double x, const SegParams &p, const float2 *kn) {
-    const float h = zc_coord(x, p.center, p.za, p.zb);
-    const float fs = floorf(h);
-    int s;
-    float fr;
-    if (!(fs > 0.0f)) {
-        s = 0;
-        fr = h > 0.0f ? h : 0.0f;
-    } else if (fs >= (float)p.kf) {
-        s = p.kf - 1;
-        fr = 1.0f;
-    } else {
-        s = (int)fs;
-        fr = h - fs;
-    }
+    // h clamped into [0, kf): below 0 -> bin 0 at fr 0, at or above kf -> the
+    // last bin at fr just below 1 (its keys keep their order: fr stays
+    // monotone); NaN (rejected by K2's screen) lands in bin 0
+    const float hmax = __int_as_float(__float_as_int((float)p.kf) - 1);  // largest float below kf
+    const float hc = fminf(fmaxf(zc_coord(x, p.center, p.za, p.zb), 0.0f), hmax);
+    const int s = (int)hc;
+    const float fr = hc - (float)s;
     const float2 az = kn[s];
-    const float lo = floorf(az.x), hi = floorf(az.y);
-    float b = floorf(fmaf(fr, az.y - az.x, az.x));
-    b = fminf(fmaxf(b, lo), hi);
+    // floor(a + fr*(z - a)) >= floor(a) always; the clamp at floor(z) keeps
+    // rounding from stepping past the next bin's first bucket
+    const float b = fminf(floorf(fmaf(fr, az.y - az.x, az.x)), floorf(az.y));
     const int bi = (int)b;
     return bi < p.k ? bi : p.k - 1;
 }

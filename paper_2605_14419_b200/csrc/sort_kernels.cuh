@@ -383,11 +383,26 @@ __global__ void k_seg_params(SegParams *segs, int nseg, const SegAcc *acc, MapCf
 // ------------------------------------------------------------------- K2
 
 constexpr int HT = 1024;  // threads of the histogram kernel (one tile per CTA)
+constexpr int CDF_KNOTS = 1024;  // coarse z-bins of the level-1 equalisation table
+
+// Keys reach the histogram through a HIST_STAGES-deep ring of TMA bulk
+// copies (HIST_CHUNK keys each, one mbarrier per stage) when the tile is
+// 16-byte aligned and the launch provided the ring (stage_ok): the copy
+// engine keeps ~128 KB per SM in flight, which per-thread loads do not.
+constexpr int HIST_CHUNK = 4096;
+constexpr int HIST_STAGES = 4;
+
+__host__ __device__ inline size_t hist_smem(int kmax, bool ring) {
+    size_t o = (size_t)((kmax + 1) & ~1) * 4 + (size_t)CDF_KNOTS * 8;
+    if (ring) o = ((o + 127) & ~(size_t)127) + (size_t)HIST_STAGES * HIST_CHUNK * 8;
+    return o;
+}
 
 template <int KK>
 __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                             uint32_t *__restrict__ mat, unsigned long long *status) {
-    extern __shared__ uint32_t hist[];
+                                             uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok) {
+    extern __shared__ __align__(128) uint32_t hist[];
+    __shared__ uint64_t full[HIST_STAGES];
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
     int64_t ti = blockIdx.x - p.tile_first;
@@ -402,27 +417,57 @@ __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restr
     float2 *cdf = (float2 *)(hist + ((p.k + 1) & ~1));
     if (p.mode == MODE_ZCDF)
         for (int q = threadIdx.x; q < p.kf; q += HT) cdf[q] = B.cdf[q];
-    __syncthreads();
     const uint64_t *src = src_keys(B, p.src);
-    int64_t i = t0 + threadIdx.x;
     // a sampled level 1 (MODE_ZCDF) has not screened the input for NaN: K2 does
     const bool screen = KK == KEY_F64 && p.mode == MODE_ZCDF && p.level == 1;
     bool nan = false;
-    auto is_nan = [](uint64_t b) { return (b << 1) > 0xFFE0000000000000ull; };
-    for (; i + 7 * HT < t1; i += 8 * HT) {
-        uint64_t b[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            if (screen) nan |= is_nan(b[u]);
-            atomicAdd(&hist[seg_bucket<KK>(b[u], p, i + u * HT, B.cuts, cdf)], 1u);
-        }
-    }
-    for (; i < t1; i += HT) {
-        const uint64_t b = __ldcs(src + i);
-        if (screen) nan |= is_nan(b);
+    auto count = [&](uint64_t b, int64_t i) {
+        if (screen) nan |= __longlong_as_double((long long)b) != __longlong_as_double((long long)b);
         atomicAdd(&hist[seg_bucket<KK>(b, p, i, B.cuts, cdf)], 1u);
+    };
+    const uint64_t *tsrc = src + t0;
+    const int64_t len = t1 - t0;
+    if (stage_ok && ((uintptr_t)tsrc & 15) == 0) {
+        uint64_t *ring = (uint64_t *)((unsigned char *)hist + (((size_t)((p.k + 1) & ~1) * 4 + (size_t)CDF_KNOTS * 8 + 127) &
+                                                                ~(size_t)127));
+        const int nch = (int)((len + HIST_CHUNK - 1) / HIST_CHUNK);
+        auto issue = [&](int c) {  // thread 0: chunk c into stage c % HIST_STAGES (whole 16-byte units)
+            const int st = c % HIST_STAGES;
+            const uint32_t bytes = (uint32_t)(min((int64_t)HIST_CHUNK, len - (int64_t)c * HIST_CHUNK) * 8) & ~15u;
+            fence_proxy_async_smem();
+            mbar_expect_tx(&full[st], bytes);
+            if (bytes) bulk_g2s(ring + (size_t)st * HIST_CHUNK, tsrc + (int64_t)c * HIST_CHUNK, bytes, &full[st]);
+        };
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < HIST_STAGES; q++) mbar_init(&full[q], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int c = 0; c < min(nch, HIST_STAGES); c++) issue(c);
+        for (int c = 0; c < nch; c++) {
+            const int st = c % HIST_STAGES;
+            mbar_wait(&full[st], (uint32_t)((c / HIST_STAGES) & 1));
+            const int64_t c0 = (int64_t)c * HIST_CHUNK;
+            const int clen = (int)min((int64_t)HIST_CHUNK, len - c0);
+            const uint64_t *kb = ring + (size_t)st * HIST_CHUNK;
+            const int cfull = clen & ~1;  // an odd last key is outside the 16-byte copy
+#pragma unroll 4
+            for (int i = threadIdx.x; i < cfull; i += HT) count(kb[i], t0 + c0 + i);
+            if (clen & 1 && threadIdx.x == 0) count(__ldcs(tsrc + c0 + clen - 1), t0 + c0 + clen - 1);
+            __syncthreads();  // stage consumed
+            if (threadIdx.x == 0 && c + HIST_STAGES < nch) issue(c + HIST_STAGES);
+        }
+    } else {
+        __syncthreads();
+        int64_t i = t0 + threadIdx.x;
+        for (; i + 7 * HT < t1; i += 8 * HT) {
+            uint64_t b[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
+#pragma unroll
+            for (int u = 0; u < 8; u++) count(b[u], i + u * HT);
+        }
+        for (; i < t1; i += HT) count(__ldcs(src + i), i);
     }
     if (__syncthreads_or(nan) && threadIdx.x == 0) *status = 3;  // ZSB_ERR_NAN
     for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
@@ -540,7 +585,6 @@ constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
 // partially written sectors that cost a DRAM read-modify-write).
 inline int scat_warps(int k, int threshold = 1024) { return k <= threshold ? 8 : 16; }
 
-constexpr int CDF_KNOTS = 1024;  // coarse z-bins of the level-1 equalisation table
 
 struct ScatLayout {
     size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, off_cdf, total;

@@ -316,11 +316,11 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
-    size_t kbytes = (size_t)((kmax + 1) & ~1) * 4 + (size_t)(CDF_KNOTS + 1) * 8;
+    const size_t kbytes = hist_smem(kmax, true);
     smem_optin(k_hist<KK>, kbytes);
     {
         PhaseScope ph(PH_HIST, c.st);
-        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS);
+        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, 1);
     }
     ZSB_LAUNCH("k_hist");
     int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
@@ -891,11 +891,11 @@ int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double
     if (key_dtype == ZSB_KEY_I64) {
         smem_optin(k_hist<0>, kb);
         k_hist<0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
-                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS);
+                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0);
     } else {
         smem_optin(k_hist<1>, kb);
         k_hist<1><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
-                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS);
+                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0);
     }
     ZSB_LAUNCH("k_hist");
     k_bucket_totals<<<(unsigned)((k + 255) / 256), 256, 0, ctx.st>>>(mat, k, ctx.P.ntiles, d_counts);
