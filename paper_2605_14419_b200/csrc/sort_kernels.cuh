@@ -13,6 +13,9 @@
 // Reference citations are /root/reference/pkg/src/zsort/<file>:<line>.
 #pragma once
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 #include "common.cuh"
 
 namespace zsb {
@@ -1083,6 +1086,237 @@ __global__ void __launch_bounds__(NT) k_sample_cdf(const uint64_t *__restrict__ 
     build_cdf_block<NT>(fine, kf, nchunks * clen, seg, p, p.za, p.zb, cdf);  // no NaN in the sample
 }
 
+// ------------------------------------------------ fused level-1 mapping
+// One cooperative launch (one CTA per SM, grid barriers between phases)
+// replaces the level-1 chain init -> sample moments -> sample CDF -> exact
+// K1 -> exact fine histogram -> CDF, which cost a launch gap each:
+//   S1  stratified sample moments (as k_sample_moments); every CTA reduces the
+//       partials itself, in the same order, so all derive identical params;
+//   S2  sample coarse-bin histogram -> CDF knots (CTA 0), mode MODE_ZCDF;
+// and, only when the sample is degenerate (NaN, all equal, no spread):
+//   E1  exact K1 over all keys (two-limb integer sum for int64 keys, shifted
+//       fp64 sums, exact ordered min/max, NaN count) -> finalize_params;
+//   E2  exact coarse-bin histogram -> CDF knots if E1 chose z-score mode.
+constexpr int LT = 512;  // threads of the fused level-1 kernel
+
+template <int KK>
+__global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ keys, int64_t n, SegParams *seg,
+                                                   int64_t *kfirst, int64_t *wfirst, int64_t nwin, int64_t k,
+                                                   int64_t tile_len, int64_t ntiles, int64_t nchunks, int64_t stride,
+                                                   SampPartial *sparts, MomPartial *mparts, unsigned int *fine,
+                                                   float2 *cdf, unsigned long long *ctrl, MapCfg mc, int kf) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t fh[KF_MAX];
+    __shared__ SampPartial wps[LT / 32];
+    __shared__ MomPartial wpm[LT / 32];
+    const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+    SegParams p{};
+    p.len = n;
+    p.tile_len = tile_len;
+    p.k = (int32_t)k;
+    p.ntiles = (int32_t)ntiles;
+    p.mode = MODE_ZSCORE;
+    p.level = 1;
+    p.center = 0.0;
+    p.std = 1.0;
+    p.scale = 1.0;
+    if (blockIdx.x == 0 && tid == 0) {
+        kfirst[0] = 0;
+        kfirst[1] = k + 1;
+        wfirst[0] = 0;
+        wfirst[1] = nwin;
+    }
+    if (blockIdx.x == 0)
+        for (int b = tid; b < kf; b += LT) fine[b] = 0u;
+    const double c0 = key_value<KK>(keys[0]);
+    const int64_t G = (int64_t)gridDim.x * LT, g0 = (int64_t)blockIdx.x * LT + tid;
+
+    // ---- S1: sample moments
+    {
+        const int64_t clen = stride < SAMP_CHUNK ? stride : SAMP_CHUNK;
+        const int64_t nitems = nchunks * SAMP_CHUNK;
+        SampPartial a{~0ull, 0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+        for (int64_t gb = g0; gb < nitems; gb += SAMP_UNROLL * G) {
+            uint64_t b[SAMP_UNROLL];
+            bool v[SAMP_UNROLL];
+#pragma unroll
+            for (int u = 0; u < SAMP_UNROLL; u++) {
+                const int64_t i = sample_pos(gb + u * G, nitems, stride, clen);
+                v[u] = i >= 0;
+                b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < SAMP_UNROLL; u++) {
+                if (!v[u]) continue;
+                const double x = key_value<KK>(b[u]);
+                if (KK == KEY_F64 && x != x) {
+                    a.nan++;
+                    continue;
+                }
+                const uint64_t o = ord_key<KK>(b[u]);
+                a.omin = o < a.omin ? o : a.omin;
+                a.omax = o > a.omax ? o : a.omax;
+                const double d = x - c0;
+                a.s1 += d;
+                a.s2 += d * d;
+                a.cnt += 1.0;
+            }
+        }
+        auto reduce = [&](SampPartial q) -> SampPartial {  // block total (valid in every thread)
+            q.omin = warp_min_u64(q.omin);
+            q.omax = warp_max_u64(q.omax);
+            q.nan = warp_sum(q.nan);
+            q.s1 = warp_sum(q.s1);
+            q.s2 = warp_sum(q.s2);
+            q.cnt = warp_sum(q.cnt);
+            __syncthreads();
+            if (lane == 0) wps[w] = q;
+            __syncthreads();
+            SampPartial t = wps[0];
+            for (int j = 1; j < LT / 32; j++) {
+                t.omin = wps[j].omin < t.omin ? wps[j].omin : t.omin;
+                t.omax = wps[j].omax > t.omax ? wps[j].omax : t.omax;
+                t.nan += wps[j].nan;
+                t.s1 += wps[j].s1;
+                t.s2 += wps[j].s2;
+                t.cnt += wps[j].cnt;
+            }
+            return t;
+        };
+        a = reduce(a);
+        if (tid == 0) sparts[blockIdx.x] = a;
+        grid.sync();
+        SampPartial q{~0ull, 0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+        if (tid < (int)gridDim.x) q = sparts[tid];  // gridDim <= LT
+        a = reduce(q);
+        bool ok = !(a.nan || a.cnt < 2.0 || a.omin == a.omax);
+        if (ok) {
+            const double mean = c0 + a.s1 / a.cnt;
+            const double dm = mean - c0;
+            double m2 = a.s2 - 2.0 * dm * a.s1 + a.cnt * dm * dm;
+            if (m2 < 0.0) m2 = 0.0;
+            const double sd = sqrt(m2 / a.cnt);
+            const double vmin = key_value<KK>(key_from_ord<KK>(a.omin)), vmax = key_value<KK>(key_from_ord<KK>(a.omax));
+            const double span = (vmax - vmin) / sd;
+            ok = sd > 0.0 && isfinite(sd) && span > 0.0 && isfinite(span);
+            if (ok) {
+                p.center = mean;
+                p.std = sd;
+                p.zmin = (mean - vmin) / sd;
+                p.scale = ((double)p.k * (1.0 - 0x1p-20)) / span;
+                ok = isfinite(p.zmin) && p.scale > 0.0 && isfinite(p.scale) && zc_coeffs(p, kf, p.za, p.zb);
+            }
+        }
+        if (ok) {
+            // ---- S2: sample coarse-bin histogram -> CDF
+            for (int b = tid; b < kf; b += LT) fh[b] = 0;
+            __syncthreads();
+            for (int64_t gb = g0; gb < nitems; gb += SAMP_UNROLL * G) {
+                uint64_t b[SAMP_UNROLL];
+                bool v[SAMP_UNROLL];
+#pragma unroll
+                for (int u = 0; u < SAMP_UNROLL; u++) {
+                    const int64_t i = sample_pos(gb + u * G, nitems, stride, clen);
+                    v[u] = i >= 0;
+                    b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < SAMP_UNROLL; u++)
+                    if (v[u]) atomicAdd(&fh[zc_bin(zc_coord(key_value<KK>(b[u]), p.center, p.za, p.zb), kf)], 1u);
+            }
+            __syncthreads();
+            for (int b = tid; b < kf; b += LT)
+                if (fh[b]) atomicAdd(&fine[b], fh[b]);
+            grid.sync();
+            if (blockIdx.x == 0) {
+                if (tid == 0) ctrl[C_SAMPLE_OK] = 1;
+                build_cdf_block<LT>(fine, kf, nchunks * clen, seg, p, p.za, p.zb, cdf);
+            }
+            return;
+        }
+    }
+
+    // ---- E1: exact K1 (the sample was degenerate)
+    MomPartial a{~0ull, 0, 0, 0, 0.0, 0.0, 0, 0};
+    for (int64_t i = g0; i < n; i += G) {
+        const uint64_t b = __ldcs(keys + i);
+        const uint64_t o = ord_key<KK>(b);
+        a.omin = o < a.omin ? o : a.omin;
+        a.omax = o > a.omax ? o : a.omax;
+        if constexpr (KK == KEY_I64) {
+            a.shi += (long long)b >> 32;
+            a.slo += b & 0xFFFFFFFFull;
+        }
+        const double x = key_value<KK>(b);
+        if (KK == KEY_F64 && x != x) {
+            a.nan++;
+        } else {
+            const double d = x - c0;
+            a.s1 += d;
+            a.s2 += d * d;
+        }
+    }
+    auto mreduce = [&](MomPartial q) -> MomPartial {
+        q.omin = warp_min_u64(q.omin);
+        q.omax = warp_max_u64(q.omax);
+        q.shi = warp_sum(q.shi);
+        q.slo = warp_sum(q.slo);
+        q.s1 = warp_sum(q.s1);
+        q.s2 = warp_sum(q.s2);
+        q.nan = warp_sum(q.nan);
+        __syncthreads();
+        if (lane == 0) wpm[w] = q;
+        __syncthreads();
+        MomPartial t = wpm[0];
+        for (int j = 1; j < LT / 32; j++) {
+            t.omin = wpm[j].omin < t.omin ? wpm[j].omin : t.omin;
+            t.omax = wpm[j].omax > t.omax ? wpm[j].omax : t.omax;
+            t.shi += wpm[j].shi;
+            t.slo += wpm[j].slo;
+            t.s1 += wpm[j].s1;
+            t.s2 += wpm[j].s2;
+            t.nan += wpm[j].nan;
+        }
+        return t;
+    };
+    a = mreduce(a);
+    if (tid == 0) mparts[blockIdx.x] = a;
+    grid.sync();
+    MomPartial q{~0ull, 0, 0, 0, 0.0, 0.0, 0, 0};
+    if (tid < (int)gridDim.x) q = mparts[tid];
+    a = mreduce(q);
+    if (a.nan) {
+        if (blockIdx.x == 0 && tid == 0) {
+            ctrl[C_STATUS] = 3;  // ZSB_ERR_NAN
+            p.mode = MODE_COPY;
+            *seg = p;
+        }
+        return;
+    }
+    const double dn = (double)n;
+    const double mean = KK == KEY_I64 ? exact_mean(a.shi, a.slo, (uint32_t)n) : c0 + a.s1 / dn;
+    const double dm = mean - c0;
+    double m2 = a.s2 - 2.0 * dm * a.s1 + dn * dm * dm;
+    if (m2 < 0.0) m2 = 0.0;
+    p.center = mean;
+    finalize_params<KK>(p, m2 / dn, a.omin, a.omax, mc, (blockIdx.x == 0 && tid == 0) ? ctrl : nullptr);
+    float za = 0.f, zb = 0.f;
+    if (p.mode != MODE_ZSCORE || mc.mapping != 0 || !zc_coeffs(p, kf, za, zb)) {
+        if (blockIdx.x == 0 && tid == 0) *seg = p;
+        return;
+    }
+    // ---- E2: exact coarse-bin histogram -> CDF
+    for (int b = tid; b < kf; b += LT) fh[b] = 0;
+    __syncthreads();
+    for (int64_t i = g0; i < n; i += G)
+        atomicAdd(&fh[zc_bin(zc_coord(key_value<KK>(__ldcs(keys + i)), p.center, za, zb), kf)], 1u);
+    __syncthreads();
+    for (int b = tid; b < kf; b += LT)
+        if (fh[b]) atomicAdd(&fine[b], fh[b]);
+    grid.sync();
+    if (blockIdx.x == 0) build_cdf_block<LT>(fine, kf, n, seg, p, za, zb, cdf);
+}
+
 // ------------------------------------------------------------ classify
 // Bucket totals of a partition level -> finish runs and next-level segments.
 // k_bstart: one thread per (segment, bucket slot): absolute bucket starts into
@@ -1110,12 +1344,11 @@ __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64
     return lo;
 }
 
-__global__ void k_bstart(const SegParams *__restrict__ segs, int nseg, const int64_t *__restrict__ kfirst,
-                         const uint32_t *__restrict__ mat, int64_t *__restrict__ bstart, SegParams *children,
-                         SegAcc *acc, unsigned long long *ctrl, ClassCfg cc, int64_t total_slots, Buffers B,
-                         int key_kind) {
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= total_slots) return;
+__device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restrict__ segs, int nseg,
+                                            const int64_t *__restrict__ kfirst, const uint32_t *__restrict__ mat,
+                                            int64_t *__restrict__ bstart, SegParams *children, SegAcc *acc,
+                                            unsigned long long *ctrl, const ClassCfg &cc, const Buffers &B,
+                                            int key_kind) {
     const int s = seg_of_slot(kfirst, nseg, g);
     const SegParams &p = segs[s];
     const int b = (int)(g - kfirst[s]);
@@ -1166,11 +1399,10 @@ __device__ __forceinline__ int lower_bound_i64(const int64_t *a, int n, int64_t 
     return lo;
 }
 
-__global__ void k_windows(const SegParams *__restrict__ segs, int nseg, const int64_t *__restrict__ kfirst,
-                          const int64_t *__restrict__ wfirst, const int64_t *__restrict__ bstart, Entry *entries,
-                          unsigned long long *ctrl, ClassCfg cc, int64_t total_windows) {
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= total_windows) return;
+__device__ __forceinline__ void window_item(int64_t g, const SegParams *__restrict__ segs, int nseg,
+                                            const int64_t *__restrict__ kfirst, const int64_t *__restrict__ wfirst,
+                                            const int64_t *__restrict__ bstart, Entry *entries,
+                                            unsigned long long *ctrl, const ClassCfg &cc) {
     const int s = seg_of_slot(wfirst, nseg, g);
     const SegParams &p = segs[s];
     if (p.mode == MODE_COPY) return;
@@ -1201,10 +1433,9 @@ __global__ void k_windows(const SegParams *__restrict__ segs, int nseg, const in
 // (single CTA; the child count is read from the control block).  k is sized
 // to the child so its buckets average ~cap/4 records (the reference's fixed
 // k across levels is a CPU choice, core.py:355).
-__global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned long long *nseg_ptr, int64_t *kfirst,
-                                               int64_t *wfirst, unsigned long long *ctrl, int32_t cap, int32_t half,
-                                               int32_t kmax_child, int32_t min_tile) {
-    const int nseg = (int)*nseg_ptr;
+__device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, int64_t *kfirst, int64_t *wfirst,
+                           unsigned long long *ctrl, int32_t cap, int32_t half, int32_t kmax_child, int32_t min_tile) {
+    const int nseg = (int)*(volatile const unsigned long long *)nseg_ptr;
     constexpr int NV = 4;  // tiles, matrix entries, records, bucket slots, windows -> 5 with windows
     __shared__ long long sh[5][32];
     __shared__ long long carry[5];
@@ -1276,6 +1507,27 @@ __global__ void __launch_bounds__(1024) k_plan(SegParams *segs, const unsigned l
         kfirst[nseg] = carry[3];
         wfirst[nseg] = carry[4];
     }
+}
+
+// Classify, one cooperative launch (1024-thread CTAs, grid barriers): bucket
+// starts and child segments, then finish windows, then (CTA 0) the plan of
+// the next level -- which rewrites kfirst/wfirst, hence the second barrier.
+__global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__ segs, int nseg, int64_t *kfirst,
+                                                   int64_t *wfirst, const uint32_t *__restrict__ mat, int64_t *bstart,
+                                                   SegParams *children, SegAcc *acc, Entry *entries,
+                                                   unsigned long long *ctrl, ClassCfg cc, int64_t total_slots,
+                                                   int64_t total_windows, Buffers B, int key_kind, int32_t kmax_child,
+                                                   int32_t min_tile) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t G = (int64_t)gridDim.x * blockDim.x, g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t g = g0; g < total_slots; g += G)
+        bstart_slot(g, segs, nseg, kfirst, mat, bstart, children, acc, ctrl, cc, B, key_kind);
+    grid.sync();
+    for (int64_t g = g0; g < total_windows; g += G)
+        window_item(g, segs, nseg, kfirst, wfirst, bstart, entries, ctrl, cc);
+    grid.sync();
+    if (blockIdx.x == 0)
+        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, cc.half, kmax_child, min_tile);
 }
 
 // ------------------------------------------------------------------- K5

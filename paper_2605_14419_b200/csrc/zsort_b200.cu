@@ -507,43 +507,46 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     MapCfg mc{cfg.mapping, (int32_t)cfg.depth_guard};
     ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping};
     const int64_t nwin1 = (n + c.P.half - 1) / c.P.half;
-    {
-        PhaseScope ph(PH_MISC, c.st);
-        k_init_level1<<<1, 1, 0, c.st>>>(seg_cur, kfirst, wfirst, nwin1, n, c.P.k, c.P.tile_len, c.P.ntiles, 0, 0.0,
-                                         1.0, 0.0, 1.0, MODE_ZSCORE);
-    }
-    ZSB_LAUNCH("k_init_level1");
     const bool equalize = cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0);
     unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
-    if (equalize) ZSB_CUDA(cudaMemsetAsync(fine, 0, (size_t)KF_MAX * 4, c.st));
+    float2 *cdf_tab = (float2 *)(c.ws + c.L.lut);
     if (equalize && !env_int("ZSB_NO_SAMPLE", 0)) {
-        // sampled level-1 mapping; on a degenerate sample the exact K1 path below runs
-        const int64_t nchunks = std::min<int64_t>(SAMP_CHUNKS_MAX, (n + SAMP_CHUNK - 1) / SAMP_CHUNK);
-        const int64_t stride = n / nchunks;
-        const int sgrid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((int64_t)num_sms() * MOM_GRID_PER_SM,
-                                 (nchunks * SAMP_CHUNK + NT * SAMP_UNROLL - 1) / (NT * SAMP_UNROLL)));
-        PhaseScope ph(PH_MOMENTS, c.st, 2);
-        k_sample_moments<KK><<<sgrid, NT, 0, c.st>>>(c.B.in_k, n, nchunks, stride, (SampPartial *)(c.ws + c.L.parts),
-                                                     ctrl, seg_cur, KF_MAX);
-        k_sample_cdf<KK><<<sgrid, NT, 0, c.st>>>(c.B.in_k, n, nchunks, stride, fine, ctrl, seg_cur, KF_MAX,
-                                                 (float2 *)(c.ws + c.L.lut));
-    }
-    int grid = std::max(1, std::min<int>(num_sms() * MOM_GRID_PER_SM, (int)((n + NT - 1) / NT)));
-    {
+        // fitted mapping: one cooperative launch maps level 1 (sampled, exact fallback)
+        int64_t nchunks = std::min<int64_t>(SAMP_CHUNKS_MAX, (n + SAMP_CHUNK - 1) / SAMP_CHUNK);
+        int64_t stride = n / nchunks;
+        const uint64_t *keys = c.B.in_k;
+        int64_t n_ = n, k_ = c.P.k, tl = c.P.tile_len, nt = c.P.ntiles, nw = nwin1;
+        SampPartial *sparts = (SampPartial *)(c.ws + c.L.parts);
+        MomPartial *mparts = (MomPartial *)(c.ws + c.L.parts) + 2 * num_sms();
+        int kf = KF_MAX;
+        void *args[] = {&keys, &n_, &seg_cur, &kfirst, &wfirst, &nw, &k_, &tl, &nt, &nchunks, &stride,
+                        &sparts, &mparts, &fine, &cdf_tab, &ctrl, &mc, &kf};
         PhaseScope ph(PH_MOMENTS, c.st);
-        k_moments<KK><<<grid, NT, 0, c.st>>>(c.B.in_k, n, (MomPartial *)(c.ws + c.L.parts), ctrl, seg_cur, mc,
-                                             nullptr);
-    }
-    ZSB_LAUNCH("k_moments");
-    if (equalize) {
-        // exact histogram equalisation of level 1 (acts only if K1 ran and chose z-score mode)
+        ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_level1_map<KK>, dim3(num_sms()), dim3(LT), args, 0, c.st));
+    } else {
         {
-            PhaseScope ph(PH_MOMENTS, c.st, 2);
-            k_fine_hist<KK><<<num_sms() * 2, 512, (size_t)KF_MAX * 4, c.st>>>(c.B.in_k, n, seg_cur, KF_MAX, fine);
-            k_build_cdf<<<1, 1024, 0, c.st>>>(fine, KF_MAX, n, seg_cur, (float2 *)(c.ws + c.L.lut));
+            PhaseScope ph(PH_MISC, c.st);
+            k_init_level1<<<1, 1, 0, c.st>>>(seg_cur, kfirst, wfirst, nwin1, n, c.P.k, c.P.tile_len, c.P.ntiles, 0,
+                                             0.0, 1.0, 0.0, 1.0, MODE_ZSCORE);
         }
-        ZSB_LAUNCH("k_fine_hist/k_build_cdf");
+        ZSB_LAUNCH("k_init_level1");
+        if (equalize) ZSB_CUDA(cudaMemsetAsync(fine, 0, (size_t)KF_MAX * 4, c.st));
+        int grid = std::max(1, std::min<int>(num_sms() * MOM_GRID_PER_SM, (int)((n + NT - 1) / NT)));
+        {
+            PhaseScope ph(PH_MOMENTS, c.st);
+            k_moments<KK><<<grid, NT, 0, c.st>>>(c.B.in_k, n, (MomPartial *)(c.ws + c.L.parts), ctrl, seg_cur, mc,
+                                                 nullptr);
+        }
+        ZSB_LAUNCH("k_moments");
+        if (equalize) {
+            // exact histogram equalisation of level 1 (acts only if K1 chose z-score mode)
+            {
+                PhaseScope ph(PH_MOMENTS, c.st, 2);
+                k_fine_hist<KK><<<num_sms() * 2, 512, (size_t)KF_MAX * 4, c.st>>>(c.B.in_k, n, seg_cur, KF_MAX, fine);
+                k_build_cdf<<<1, 1024, 0, c.st>>>(fine, KF_MAX, n, seg_cur, cdf_tab);
+            }
+            ZSB_LAUNCH("k_fine_hist/k_build_cdf");
+        }
     }
 
     int nseg = 1;
@@ -564,16 +567,17 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         if (rc) return rc;
         ZSB_CUDA(cudaMemsetAsync(ctrl + C_NCHILD, 0, 16, c.st));  // C_NCHILD, C_NENTRY
         {
-            PhaseScope ph(PH_CLASSIFY, c.st, 3);
-            k_bstart<<<(unsigned)((total_slots + 255) / 256), 256, 0, c.st>>>(seg_cur, nseg, kfirst, mat, bstart,
-                                                                             seg_next, acc, ctrl, cc, total_slots,
-                                                                             c.B, KK);
-            k_windows<<<(unsigned)((total_windows + 255) / 256), 256, 0, c.st>>>(seg_cur, nseg, kfirst, wfirst, bstart,
-                                                                               entries, ctrl, cc, total_windows);
-            k_plan<<<1, 1024, 0, c.st>>>(seg_next, ctrl + C_NCHILD, kfirst, wfirst, ctrl, (int32_t)c.P.cap,
-                                         (int32_t)c.P.half, KMAX_CHILD, MIN_TILE);
+            PhaseScope ph(PH_CLASSIFY, c.st);
+            const int64_t need = std::max<int64_t>(1, (std::max(total_slots, total_windows) + 1023) / 1024);
+            const int cgrid = (int)std::min<int64_t>(need, (int64_t)num_sms());
+            int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = MIN_TILE;
+            int64_t ts = total_slots, tw = total_windows;
+            Buffers Bv = c.B;
+            void *args[] = {&seg_cur, &nseg_, &kfirst, &wfirst, &mat, &bstart, &seg_next, &acc, &entries, &ctrl,
+                            &cc, &ts, &tw, &Bv, &key_kind, &kmc, &mt};
+            ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_classify, dim3(cgrid), dim3(1024), args, 0, c.st));
         }
-        ZSB_LAUNCH("k_bstart/k_windows/k_plan");
+        ZSB_LAUNCH("k_classify");
         // The host needs this level's outcome (children, sizes of the next
         // level); the finish of this level does not: it is enqueued before the
         // host waits (count on the device), so the GPU goes straight on.

@@ -278,6 +278,25 @@ class TestEdgeCases:
         f[::1000] = 1e300
         assert_matches_oracle(Z, f)
 
+    def test_sample_blind_spots(self, Z):
+        # The fitted level 1 maps from a stratified sample (runs of 32 keys every
+        # n/8192 positions).  Keys that agree on every sampled position but not
+        # elsewhere force the exact fallback; a NaN outside the sample must
+        # still be rejected (K2 screens every key).
+        n = 1 << 20
+        stride = n // 8192
+        pos = np.arange(n)
+        sampled = (pos % stride) < 32
+        rng = np.random.default_rng(11)
+        keys = np.where(sampled, 0, rng.integers(-10**6, 10**6, size=n)).astype(np.int64)
+        assert_matches_oracle(Z, keys)
+        f = np.where(sampled, 1.5, rng.standard_normal(n))
+        assert_matches_oracle(Z, f)
+        g = rng.standard_normal(n)
+        g[np.flatnonzero(~sampled)[12345]] = np.nan
+        with pytest.raises(ValueError):
+            Z.zsort(g)
+
     def test_nondefault_thresholds(self, Z):  # test_zsort.py:107-114
         keys = np.random.default_rng(42).integers(-10**10, 10**10, size=50_000, dtype=np.int64)
         for cfg in (Z.SortConfig(insertion_threshold=1, counting_range_threshold=1), Z.SortConfig(depth_guard=3),
