@@ -12,6 +12,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --log-file gpurun_out/${TAG}_launches.csv $CMD > /dev/null 2>&1
 echo "launch list rc=$?"
 $CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_finish|k_hist|k_moments" -s 8 -c 6 \
+ncu --set full --clock-control none --import-source on -k regex:"k_level1_map|k_hist|k_scatter|k_classify|k_finish" -s 12 -c 6 \
     -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?"
