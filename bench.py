@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--mapping", default="fitted", choices=["fitted", "paper"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-comparators", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -342,12 +343,43 @@ def main():
                        "api": "paper_2605_14419_b200.zsort(pinned host tensors, out=pinned host tensors)"}
         if not (np.array_equal(hok.numpy(), out_k.cpu().numpy()) and np.array_equal(hop.numpy(), out_p.cpu().numpy())):
             raise SystemExit("e2e output differs from the device-resident run")
+    if not args.no_comparators:
+        line["comparators"] = comparators(d_keys, d_pay, out_k, out_p, flush, stream, args.steps, ms_per_step)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(keys_h, pay_h)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def comparators(d_keys, d_pay, out_k, out_p, flush, stream, steps, ms_ours):
+    """SURVEY §8(f)3, the paper's bit-width-wall contrast on the GPU: the same
+    stable sort (keys + payload permuted alongside) with torch.sort(stable=True)
+    -- CUB's LSD radix sort, one pass per 8-bit digit of the 64-bit key -- plus
+    the payload gather, same inputs, same L2 flush and CUDA-event timing.  The
+    outputs are checked equal to ours."""
+    import torch
+
+    def run():
+        k, perm = torch.sort(d_keys, stable=True)
+        return k, d_pay[perm]
+
+    k, p = run()
+    same = bool(torch.equal(k.view(torch.int64), out_k.view(torch.int64)) and torch.equal(p, out_p))
+    ms = []
+    for _ in range(max(3, steps)):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = sum(ms) / len(ms)
+    return {"torch.sort(stable=True)+gather": {"ms_per_step": t, "keys_per_s": d_keys.numel() / (t / 1e3),
+                                               "ours_speedup": t / ms_ours, "same_output": same}}
 
 
 def run_dist(args, rank, world, dev):

@@ -1690,6 +1690,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     mbar_wait(bar, parity);
     parity ^= 1u;
     __syncthreads();
+    FIN_MARK(7);  // staged
 
     uint64_t o[F];
 #pragma unroll

@@ -366,17 +366,18 @@ void fin_prof_dump() {
     if (!g_fin_prof) return;
     std::vector<long long> h((size_t)g_fin_prof_n * 8);
     cudaMemcpy(h.data(), g_fin_prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    double acc[7] = {0};
+    double acc[8] = {0};
     int64_t cnt = 0;
     for (int64_t b = 0; b < g_fin_prof_n; b++) {
         const long long *t = &h[(size_t)b * 8];
         if (!t[6]) continue;  // all-equal or empty runs exit early
         cnt++;
         for (int q = 1; q <= 6; q++) acc[q] += (double)(t[q] - t[q - 1]);
+        acc[7] += (double)(t[7] - t[0]);
     }
-    fprintf(stderr, "[zsb] finish phases over %lld CTAs (cycles): load %.0f minmax+params %.0f hist %.0f scan %.0f "
-                    "place %.0f rank+store %.0f\n", (long long)cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
-            acc[5] / cnt, acc[6] / cnt);
+    fprintf(stderr, "[zsb] finish phases over %lld runs (cycles): load %.0f (staged after %.0f) minmax+params %.0f "
+                    "hist %.0f scan %.0f place %.0f rank+store %.0f\n", (long long)cnt, acc[1] / cnt, acc[7] / cnt,
+            acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
     cudaFree(g_fin_prof);
     g_fin_prof = nullptr;
     g_fin_prof_n = 0;

@@ -348,3 +348,19 @@ def test_config5_shape_structural_single_gpu(Z):
     ok, op, _ = Z.zsort(hk, np.arange(hk.size, dtype=np.int64))
     ek, ep, _ = O.stable_sort(hk, np.arange(hk.size, dtype=np.int64))
     assert np.array_equal(ok, ek) and np.array_equal(op, ep)
+
+
+# ------------------------------------------------ bench seam
+
+def test_harness_seam(Z):
+    from paper_2605_14419_b200 import harness
+
+    registry = {}
+    name = harness.register(lambda n, a: registry.__setitem__(n, a))
+    keys = O.generate_family("uniform", 50_000, 9)
+    pay = np.arange(keys.size, dtype=np.int64)[::-1].copy()
+    k, p = registry[name](keys.copy(), pay.copy(), None)
+    ek, ep, _ = O.stable_sort(keys, pay)
+    assert np.array_equal(k, ek) and np.array_equal(p, ep)
+    r = harness.run_trial_gpu(keys, pay.astype(np.int32), repetitions=3)
+    assert r.verified and r.size == keys.size and r.min_ms > 0

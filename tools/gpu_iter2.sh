@@ -3,7 +3,7 @@ timeout -s KILL 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu
 tail -3 gpurun_out/pytest_gpu.log
 timeout -s KILL 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 tail -2 gpurun_out/bench.log | cut -c1-1500
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-comparators"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
     --log-file gpurun_out/launches.csv $CMD > /dev/null 2>&1
