@@ -1555,15 +1555,15 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
 // output store, so src may alias the output (in-place refinement).
 
 constexpr int FIN_INS = 32;         // sub-buckets up to this size are ranked by comparison
-constexpr int FIN_SBITS_MAX = 14;   // <= 16384 sub-buckets (16-bit cursors)
-constexpr int FIN_BIG_MAX = 512;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
+constexpr int FIN_SBITS_MAX = 13;   // <= 8192 sub-buckets (16-bit cursors)
+constexpr int FIN_BIG_MAX = 384;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
 
-constexpr int FT = 512;         // threads per finish CTA
+constexpr int FT = 1024;        // threads per finish CTA
 constexpr int FW = FT / 32;     // warps per finish CTA
 
 template <int PB>
 struct FinItems {
-    static constexpr int F = PB == 8 ? 16 : 24;  // records per thread; cap = FT * F
+    static constexpr int F = PB == 8 ? 8 : 12;  // records per thread; cap = FT * F
 };
 
 struct FinLayout {
@@ -1732,13 +1732,8 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             __syncthreads();
         }
     }
-    omin = r_min[0];
-    omax = r_max[0];
-#pragma unroll
-    for (int j = 1; j < FW; j++) {
-        omin = min(omin, r_min[j]);
-        omax = max(omax, r_max[j]);
-    }
+    omin = warp_min_u64(lane < FW ? r_min[lane] : ~0ull);  // every warp reduces the warp partials itself
+    omax = warp_max_u64(lane < FW ? r_max[lane] : 0ull);
     auto key_bits = [&](uint64_t ov, int idx) -> uint64_t {
         uint64_t kb = key_from_ord<KK>(ov);
         if (KK == KEY_F64 && anyneg && ((negzero[idx >> 5] >> (idx & 31)) & 1u)) kb = SIGN;
@@ -1777,10 +1772,12 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     // positive constant keep the digit monotone in the key.
     bool vdig = false;
     double vlo = 0.0, vinv = 0.0;
+    __shared__ double s_vinv;
     if constexpr (KK == KEY_F64) {
         const double lo = key_value<KK>(key_from_ord<KK>(omin)), hi = key_value<KK>(key_from_ord<KK>(omax));
         const double span = __dsub_rn(hi, lo);
-        vinv = (double)S / span;
+        if (tid == 0) s_vinv = (double)S / span;  // one fp64 division, read after the barrier below
+        vinv = 1.0;
 #ifndef ZSB_FIN_VDIG
 #define ZSB_FIN_VDIG 1
 #endif
@@ -1798,6 +1795,10 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
     for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
     __syncthreads();
+    if constexpr (KK == KEY_F64) {
+        vinv = s_vinv;
+        vdig = vdig && isfinite(vinv);
+    }
     FIN_MARK(2);
     // ---- histogram (16-bit counters: no carry, counts <= cap < 2^16)
     uint32_t dpk[(F + 1) / 2];  // digits, two per register
