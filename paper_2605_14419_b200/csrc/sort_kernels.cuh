@@ -660,7 +660,7 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
 template <int KK, int PB, int SW>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
-                                                              int dst_sel, long long *prof) {
+                                                              int dst_sel, long long *prof, int tie_check) {
 #ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
     long long t_mark = prof ? clock64() : 0;
     long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
@@ -764,12 +764,14 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
             uint32_t *word = (uint32_t *)cnt + (q >> 1);
             if (bkj >= 0) {
                 old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
-                after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
+                if (tie_check) after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
             }
-            const bool tie = bkj >= 0 && after != old + 1u;
-            if (__any_sync(0xffffffffu, tie)) {
-                const unsigned m = __match_any_sync(0xffffffffu, bkj);
-                if (bkj >= 0 && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
+            if (tie_check) {
+                const bool tie = bkj >= 0 && after != old + 1u;
+                if (__any_sync(0xffffffffu, tie)) {
+                    const unsigned m = __match_any_sync(0xffffffffu, bkj);
+                    if (bkj >= 0 && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
+                }
             }
             pk[j] = bkj >= 0 ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
             const int i = threadIdx.x + j * ST;
@@ -827,6 +829,33 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         for (int q = 0; q < 6; q++) prof[(int64_t)blockIdx.x * 8 + q] = acc_ph[q];
 #endif
 #undef SCAT_MARK
+}
+
+// Probe (once per device, at first use): do the lanes of one warp that hit
+// the same shared-memory word with atomicAdd receive their old values in lane
+// order?  sm_100 does (0 violations in millions of tie groups), and then
+// k_scatter skips its tie detection; any violation keeps it on.
+__global__ void k_probe_atomic_order(const uint32_t seed, unsigned long long *viol) {
+    __shared__ uint32_t cnt[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    unsigned long long v = 0;
+    uint32_t r = seed ^ (threadIdx.x * 0x9E3779B9u);
+    for (int it = 0; it < 256; it++) {
+        r = r * 1664525u + 1013904223u;
+        const int nb = 2 << (it & 5);  // 2 .. 64 buckets
+        const int b = (int)((r >> 8) % (uint32_t)nb);
+        const int q = w * 64 + b;  // per-(warp, bucket) u16 counter, two per word
+        const uint32_t sh = 16 * (q & 1);
+        const uint32_t old = (atomicAdd(&cnt[q >> 1], 1u << sh) >> sh) & 0xFFFFu;
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        for (int l = 0; l < 32; l++) {
+            const uint32_t o2 = __shfl_sync(0xffffffffu, old, l);
+            v += ((m >> l) & 1u) && l < lane && o2 > old;
+        }
+    }
+    if (v) atomicAdd(viol, v);
 }
 
 // ------------------------------------------------------- equalisation

@@ -310,6 +310,33 @@ void scat_prof_dump() {
     g_scat_prof_n = 0;
 }
 
+// 1 if the scatter must detect same-bucket lanes of one atomic instruction
+// (shared atomics not handed out in lane order on this device); probed once
+// per device.  ZSB_TIE_CHECK=0/1 overrides.
+int scatter_tie_check() {
+    static int dev_flag[64];
+    static bool probed[64] = {false};
+    static std::mutex mu;
+    const int forced = env_int("ZSB_TIE_CHECK", -1);
+    if (forced >= 0) return forced ? 1 : 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 1;
+    std::lock_guard<std::mutex> g(mu);
+    if (!probed[dev]) {
+        unsigned long long *d = nullptr, h = 1;
+        if (cudaMalloc(&d, 8) == cudaSuccess) {
+            cudaMemset(d, 0, 8);
+            k_probe_atomic_order<<<8, 512>>>(0x1234567u, d);
+            if (cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost) != cudaSuccess) h = 1;
+            cudaFree(d);
+        }
+        dev_flag[dev] = h ? 1 : 0;
+        probed[dev] = true;
+    }
+    return dev_flag[dev];
+}
+
 template <int KK, int PB>
 int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
                      bool segs_level1 = false) {
@@ -338,12 +365,14 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 8>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 8><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
+        k_scatter<KK, PB, 8><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles),
+                                                                    scatter_tie_check());
     } else {
         const size_t sbytes = scat_layout(kmax, PB, 16).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 16>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 16><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
+        k_scatter<KK, PB, 16><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles),
+                                                                     scatter_tie_check());
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;

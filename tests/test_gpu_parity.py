@@ -364,3 +364,16 @@ def test_harness_seam(Z):
     assert np.array_equal(k, ek) and np.array_equal(p, ep)
     r = harness.run_trial_gpu(keys, pay.astype(np.int32), repetitions=3)
     assert r.verified and r.size == keys.size and r.min_ms > 0
+
+
+@pytest.mark.parametrize("tie_check", ["0", "1"])
+def test_scatter_tie_paths(Z, tie_check, monkeypatch):
+    # the scatter ranks items with shared atomics; lanes of one instruction
+    # that share a bucket are either trusted to the device's lane order (probed
+    # at first use) or detected and re-ranked: both paths must be stable
+    monkeypatch.setenv("ZSB_TIE_CHECK", tie_check)
+    rng = np.random.default_rng(77)
+    few = rng.integers(0, 50, size=2_000_000).astype(np.int64)
+    assert_matches_oracle(Z, few)
+    runs = np.repeat(rng.standard_normal(20_000), 100)  # sorted-run-like ties inside warps
+    assert_matches_oracle(Z, runs)
