@@ -403,9 +403,19 @@ __host__ __device__ inline size_t hist_smem(int kmax, bool ring) {
 
 template <int KK>
 __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                             uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok) {
+                                             uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok,
+                                             unsigned long long *scan_status, int scan_words,
+                                             unsigned long long *ctrl) {
     extern __shared__ __align__(128) uint32_t hist[];
     __shared__ uint64_t full[HIST_STAGES];
+    if (blockIdx.x == 0 && ctrl) {  // state of the kernels that follow (saves separate memsets)
+        for (int q = threadIdx.x; q < scan_words; q += HT) scan_status[q] = 0ull;
+        if (threadIdx.x == 0) {
+            ctrl[C_SCAN_TICKET] = 0ull;
+            ctrl[C_NCHILD] = 0ull;
+            ctrl[C_NENTRY] = 0ull;
+        }
+    }
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
     int64_t ti = blockIdx.x - p.tile_first;
@@ -1155,8 +1165,10 @@ __global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ 
         wfirst[0] = 0;
         wfirst[1] = nwin;
     }
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0) {
         for (int b = tid; b < kf; b += LT) fine[b] = 0u;
+        if (tid < C_SLOTS) ctrl[tid] = 0ull;  // fresh control block (nothing reads it before the first barrier)
+    }
     const double c0 = key_value<KK>(keys[0]);
     const int64_t G = (int64_t)gridDim.x * LT, g0 = (int64_t)blockIdx.x * LT + tid;
 
@@ -1428,33 +1440,31 @@ __device__ __forceinline__ int lower_bound_i64(const int64_t *a, int n, int64_t 
     return lo;
 }
 
-__device__ __forceinline__ void window_item(int64_t g, const SegParams *__restrict__ segs, int nseg,
-                                            const int64_t *__restrict__ kfirst, const int64_t *__restrict__ wfirst,
-                                            const int64_t *__restrict__ bstart, Entry *entries,
-                                            unsigned long long *ctrl, const ClassCfg &cc) {
+// Finish runs of window g (its buckets whose start lies in the window): up to
+// two entries, returned in e[] (count in the result); the caller appends them.
+__device__ __forceinline__ int window_item(int64_t g, const SegParams *__restrict__ segs, int nseg,
+                                           const int64_t *__restrict__ kfirst, const int64_t *__restrict__ wfirst,
+                                           const int64_t *__restrict__ bstart, const ClassCfg &cc,
+                                           const int64_t *bs_one, Entry e[2]) {
     const int s = seg_of_slot(wfirst, nseg, g);
     const SegParams &p = segs[s];
-    if (p.mode == MODE_COPY) return;
+    if (p.mode == MODE_COPY) return 0;
     const int64_t w = g - wfirst[s];
-    const int64_t *bs = bstart + kfirst[s];  // k + 1 slots
+    const int64_t *bs = bs_one ? bs_one : bstart + kfirst[s];  // k + 1 slots (a shared copy for one segment)
     const int64_t ws = p.start + w * cc.half, we = ws + cc.half;
     const int b0 = lower_bound_i64(bs, p.k, ws);
     const int b1 = lower_bound_i64(bs, p.k, we);
-    if (b0 >= b1) return;  // no bucket starts inside this window
+    if (b0 >= b1) return 0;  // no bucket starts inside this window
     const int dst = (p.src == 1) ? 2 : 1;
     const int64_t last = bs[b1] - bs[b1 - 1];
     int64_t e0 = bs[b0], e1 = bs[b1];
+    int ne = 0;
     if (last > cc.half) {
         e1 = bs[b1 - 1];
-        if (last <= cc.cap) {  // a mid-size bucket is a run of its own
-            unsigned long long e = atomicAdd(&ctrl[C_NENTRY], 1ull);
-            entries[e] = Entry{bs[b1 - 1], (int32_t)last, dst};
-        }
+        if (last <= cc.cap) e[ne++] = Entry{bs[b1 - 1], (int32_t)last, dst};  // a mid-size bucket is a run of its own
     }
-    if (e1 > e0) {
-        unsigned long long e = atomicAdd(&ctrl[C_NENTRY], 1ull);
-        entries[e] = Entry{e0, (int32_t)(e1 - e0), dst};
-    }
+    if (e1 > e0) e[ne++] = Entry{e0, (int32_t)(e1 - e0), dst};
+    return ne;
 }
 
 // ----------------------------------------------------------------- plan
@@ -1546,14 +1556,42 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
                                                    SegParams *children, SegAcc *acc, Entry *entries,
                                                    unsigned long long *ctrl, ClassCfg cc, int64_t total_slots,
                                                    int64_t total_windows, Buffers B, int key_kind, int32_t kmax_child,
-                                                   int32_t min_tile) {
+                                                   int32_t min_tile, unsigned long long *ref_zero) {
     cg::grid_group grid = cg::this_grid();
+    if (blockIdx.x == 0 && threadIdx.x < 4 && ref_zero) ref_zero[threadIdx.x] = 0ull;  // the finish's refine counts/tickets
     const int64_t G = (int64_t)gridDim.x * blockDim.x, g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t g = g0; g < total_slots; g += G)
         bstart_slot(g, segs, nseg, kfirst, mat, bstart, children, acc, ctrl, cc, B, key_kind);
     grid.sync();
-    for (int64_t g = g0; g < total_windows; g += G)
-        window_item(g, segs, nseg, kfirst, wfirst, bstart, entries, ctrl, cc);
+    // one segment (level 1): every CTA binary-searches a shared copy of its bucket starts
+    constexpr int BS_SHARED = 2049;
+    __shared__ int64_t bs_sh[BS_SHARED];
+    const int64_t *bs_one = nullptr;
+    if (nseg == 1 && segs[0].k + 1 <= BS_SHARED) {
+        for (int q = threadIdx.x; q <= segs[0].k; q += blockDim.x) bs_sh[q] = bstart[kfirst[0] + q];
+        __syncthreads();
+        bs_one = bs_sh;
+    }
+    // windows: whole warps iterate together so each warp appends its entries
+    // with one atomic (the entry counter is otherwise a hot spot)
+    const int lane = lane_id();
+    for (int64_t gw = g0 - lane; gw < total_windows; gw += G) {
+        Entry e[2];
+        const int ne = gw + lane < total_windows
+                           ? window_item(gw + lane, segs, nseg, kfirst, wfirst, bstart, cc, bs_one, e)
+                           : 0;
+        int pre = ne;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, pre, 31);
+        unsigned long long base = 0;
+        if (lane == 31 && tot) base = atomicAdd(&ctrl[C_NENTRY], (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        for (int q = 0; q < ne; q++) entries[base + pre - ne + q] = e[q];
+    }
     grid.sync();
     if (blockIdx.x == 0)
         plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, cc.half, kmax_child, min_tile);

@@ -345,14 +345,13 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
     const size_t kbytes = hist_smem(kmax, true);
     smem_optin(k_hist<KK>, kbytes);
+    const int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
     {
         PhaseScope ph(PH_HIST, c.st);
-        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, 1);
+        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, 1, status,
+                                                         (int)(sblocks + 1), ctrl);
     }
     ZSB_LAUNCH("k_hist");
-    int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
-    ZSB_CUDA(cudaMemsetAsync(status, 0, (size_t)(sblocks + 1) * 8, c.st));
-    ZSB_CUDA(cudaMemsetAsync(ctrl + C_SCAN_TICKET, 0, 8, c.st));
     {
         PhaseScope ph(PH_SCAN, c.st);
         k_scan<<<(unsigned)sblocks, NT, 0, c.st>>>(mat, mat_entries, status, ctrl);
@@ -476,7 +475,9 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int64_t stats[ZSB_STAT_SLOTS] = {0, 0, 0, 0, 0};
     if (int rc = host_sync_init()) return rc;
     unsigned long long *hc = g_hs.ctrl;  // pinned: the copies below are truly asynchronous
-    ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
+    const bool fused_l1 = c.n > c.P.cap && cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0) &&
+                          !env_int("ZSB_NO_SAMPLE", 0);
+    if (!fused_l1) ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));  // else k_level1_map clears it
     auto full_sync = [&]() -> int {  // control block -> host, wait for everything enqueued
         ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, c.st));
         ZSB_CUDA(cudaStreamSynchronize(c.st));
@@ -488,8 +489,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     // pass, count on the device) without a host round trip; parity `par`
     // selects the refine lists.
     auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
-                              int64_t bound, int par) -> int {
-        ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[2 * par], 0, 32, c.st));  // two counts, two tickets
+                              int64_t bound, int par, bool zeroed = false) -> int {
+        if (!zeroed) ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[2 * par], 0, 32, c.st));  // two counts, two tickets
         int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par);
         if (rc) return rc;
         return launch_finish<KK, PB>(c, (const Entry *)(c.ws + c.L.refine[2 * par]), ctrl + REF_SLOT[2 * par],
@@ -540,7 +541,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     const bool equalize = cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0);
     unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
     float2 *cdf_tab = (float2 *)(c.ws + c.L.lut);
-    if (equalize && !env_int("ZSB_NO_SAMPLE", 0)) {
+    if (fused_l1) {
         // fitted mapping: one cooperative launch maps level 1 (sampled, exact fallback)
         int64_t nchunks = std::min<int64_t>(SAMP_CHUNKS_MAX, (n + SAMP_CHUNK - 1) / SAMP_CHUNK);
         int64_t stride = n / nchunks;
@@ -595,16 +596,16 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         const int dst_sel = (level == 1) ? 1 : ((level % 2 == 0) ? 2 : 1);
         int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel, level == 1);
         if (rc) return rc;
-        ZSB_CUDA(cudaMemsetAsync(ctrl + C_NCHILD, 0, 16, c.st));  // C_NCHILD, C_NENTRY
-        {
+        {  // (C_NCHILD / C_NENTRY were cleared by K2)
             PhaseScope ph(PH_CLASSIFY, c.st);
             const int64_t need = std::max<int64_t>(1, (std::max(total_slots, total_windows) + 1023) / 1024);
             const int cgrid = (int)std::min<int64_t>(need, (int64_t)num_sms());
             int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = MIN_TILE;
             int64_t ts = total_slots, tw = total_windows;
             Buffers Bv = c.B;
+            unsigned long long *ref_zero = ctrl + REF_SLOT[2 * par];
             void *args[] = {&seg_cur, &nseg_, &kfirst, &wfirst, &mat, &bstart, &seg_next, &acc, &entries, &ctrl,
-                            &cc, &ts, &tw, &Bv, &key_kind, &kmc, &mt};
+                            &cc, &ts, &tw, &Bv, &key_kind, &kmc, &mt, &ref_zero};
             ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_classify, dim3(cgrid), dim3(1024), args, 0, c.st));
         }
         ZSB_LAUNCH("k_classify");
@@ -613,7 +614,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         // host waits (count on the device), so the GPU goes straight on.
         ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, c.st));
         ZSB_CUDA(cudaEventRecord(g_hs.ev, c.st));
-        rc = enqueue_finish(entries, ctrl + C_NENTRY, c.L.ent_cap, c.L.ent_cap, par);
+        rc = enqueue_finish(entries, ctrl + C_NENTRY, c.L.ent_cap, c.L.ent_cap, par, true);
         if (rc) return rc;
         ZSB_CUDA(cudaEventSynchronize(g_hs.ev));
         if (hc[C_STATUS] == 3) {
@@ -925,11 +926,13 @@ int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double
     if (key_dtype == ZSB_KEY_I64) {
         smem_optin(k_hist<0>, kb);
         k_hist<0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
-                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0);
+                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0,
+                                                           nullptr, 0, nullptr);
     } else {
         smem_optin(k_hist<1>, kb);
         k_hist<1><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
-                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0);
+                                                           (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0,
+                                                           nullptr, 0, nullptr);
     }
     ZSB_LAUNCH("k_hist");
     k_bucket_totals<<<(unsigned)((k + 255) / 256), 256, 0, ctx.st>>>(mat, k, ctx.P.ntiles, d_counts);
