@@ -272,27 +272,7 @@ def main():
 
     hbm_peak, peak_kind = peaks()
     rec = 8 + pb
-    alg_bytes_step = {"moments": 8 * n, "histogram": 8 * n, "scan": None, "scatter": 2 * rec * n,
-                      "classify": None, "finish": 2 * rec * n, "recursion_stats": None, "misc": None}
-    phase_ms = {name: ms_phase[i] / args.steps for i, name in enumerate(_lib.PHASES)}
-    phase_launch = {name: launches[i] / args.steps for i, name in enumerate(_lib.PHASES)}
-    dominant = max(("moments", "histogram", "scatter", "finish"), key=lambda k: phase_ms[k])
-    # the finish phase is the main launch plus its refine pass (a few runs):
-    # the algorithmic bytes are charged to the phase, over the phase's time
-    per_launch_bytes = alg_bytes_step[dominant]
-    per_launch_ms = phase_ms[dominant]
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    traffic = None  # DRAM bytes of the phase's launches from the latest committed ncu --set full capture
-    try:
-        import glob
-        tf = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
-        if tf:
-            tj = json.load(open(tf[-1]))
-            launches_b = tj["bytes_per_launch"].get(f"k_{dominant}")
-            if launches_b:
-                traffic = float(sum(launches_b[:max(1, int(round(phase_launch[dominant])))]))
-    except Exception:
-        traffic = None
+    roof, phase_ms = roofline_from_phases(n, rec, ms_phase, launches, args.steps)
     sort_alg_bytes = (16 + 4 * rec) * n
     gpu_launches = int(sum(launches[i] for i in range(8)))
     line = {
@@ -303,12 +283,7 @@ def main():
         "config": {"workload": CONFIG_DESC[args.config], "n_per_gpu": int(n), "payload_bytes": pb,
                    "mapping": args.mapping, "l2": "flushed (512 MiB write) between timed steps",
                    "parallelism": "replicas" if world > 1 else "single"},
-        "roofline": {"bound": "hbm", "kernel": f"k_{dominant}", "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "alg_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_ms,
-                     "launches_per_step": phase_launch[dominant],
-                     "note": "alg bytes = 2 x (8 + payload) per key for the phase; time = the phase's CUDA-event time "
-                             "(main launch + refine pass); DRAM traffic per launch in profiles/"},
+        "roofline": roof,
         "sort_roofline": {"alg_bytes_per_key": 16 + 4 * rec, "achieved_gbs": sort_alg_bytes / (ms_per_step / 1e3) / 1e9,
                           "frac": sort_alg_bytes / (ms_per_step / 1e3) / 1e9 / hbm_peak},
         "phases_ms_per_step": {k: round(v, 4) for k, v in phase_ms.items()},
@@ -351,6 +326,40 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def roofline_from_phases(n, rec, ms_phase, launches, steps):
+    """Roofline of the dominant phase from the library's per-phase CUDA-event
+    times (a separate pass of the same steps).  The finish phase is the main
+    launch plus its refine pass: its algorithmic bytes are charged to the
+    phase over the phase's time."""
+    from paper_2605_14419_b200 import _lib
+
+    hbm_peak, peak_kind = peaks()
+    alg_bytes_step = {"moments": 8 * n, "histogram": 8 * n, "scan": None, "scatter": 2 * rec * n,
+                      "classify": None, "finish": 2 * rec * n, "recursion_stats": None, "misc": None}
+    phase_ms = {name: ms_phase[i] / steps for i, name in enumerate(_lib.PHASES)}
+    phase_launch = {name: launches[i] / steps for i, name in enumerate(_lib.PHASES)}
+    dominant = max(("moments", "histogram", "scatter", "finish"), key=lambda k: phase_ms[k])
+    alg = alg_bytes_step[dominant]
+    ms = max(phase_ms[dominant], 1e-9)
+    achieved = alg / (ms / 1e3) / 1e9
+    traffic = None  # DRAM bytes of the phase's launches from the latest committed ncu --set full capture
+    try:
+        import glob
+        tf = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
+        if tf:
+            launches_b = json.load(open(tf[-1]))["bytes_per_launch"].get(f"k_{dominant}")
+            if launches_b:
+                traffic = float(sum(launches_b[:max(1, int(round(phase_launch[dominant])))]))
+    except Exception:
+        traffic = None
+    roof = {"bound": "hbm", "kernel": f"k_{dominant}", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
+            "launch_ms": ms, "launches_per_step": phase_launch[dominant],
+            "note": "alg bytes = 2 x (8 + payload) per key for the phase; time = the phase's CUDA-event time "
+                    "(main launch + refine pass); DRAM traffic per launch in profiles/"}
+    return roof, phase_ms
 
 
 def comparators(d_keys, d_pay, out_k, out_p, flush, stream, steps, ms_ours):
@@ -425,6 +434,24 @@ def run_dist(args, rank, world, dev):
     t = torch.tensor([sum(step_ms)], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
+    # our kernel launches per timed step and the per-phase breakdown of the
+    # local work, from a separate pass of the same steps
+    import ctypes
+    from paper_2605_14419_b200 import _lib
+    L = _lib.load()
+    ms_phase = (ctypes.c_double * 8)()
+    launches = (ctypes.c_int64 * 8)()
+    L.zsb_timing_read(ms_phase, launches, 8, 1)
+    L.zsb_timing_enable(1)
+    for _ in range(args.steps):
+        flush.zero_()
+        dist.barrier()
+        dist_zsort(dk, dp, rank * n)
+    torch.cuda.synchronize()
+    L.zsb_timing_enable(0)
+    L.zsb_timing_read(ms_phase, launches, 8, 1)
+    roof, phase_ms = roofline_from_phases(n, 12, ms_phase, launches, args.steps)
+    gpu_launches = int(sum(launches[i] for i in range(8)))
     # e2e: pinned host shard -> device -> distributed sort -> pinned host result
     hk = torch.from_numpy(keys_h).pin_memory()
     hp = torch.from_numpy(pay_h).pin_memory()
@@ -455,7 +482,8 @@ def run_dist(args, rank, world, dev):
             "exchange": {"sent_per_rank": info.get("sent"), "received_rank0": info.get("received")},
             "e2e": {"value": n * world / (float(te.item()) / 1e3), "unit": "keys/s",
                     "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * 12)},
-            "gpu_launches": None, "clocks": clk.summary(),
+            "gpu_launches": gpu_launches, "roofline": roof,
+            "phases_ms_per_step": {k: round(v, 4) for k, v in phase_ms.items()}, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -74,6 +74,12 @@ struct PhaseScope {
     }
 };
 
+// launches outside any PhaseScope (multi-GPU phases): counted under misc
+inline void count_launches(int nl) {
+    g_t.launch_total += nl;
+    g_t.launches[PH_MISC] += nl;
+}
+
 // after a stream sync: fold recorded pairs into the per-phase totals
 void timing_collect() {
     if (!g_t.on) return;
@@ -998,10 +1004,12 @@ int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double s
     int rc = check_common(d_keys, key_dtype, 0, n);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
+    count_launches(1);
     k_dist_init<<<1, 32, 0, st>>>(d_out3, (unsigned long long *)d_out_bits2);
     ZSB_LAUNCH("k_dist_init");
     if (n == 0) return ZSB_OK;
     const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    count_launches(1);
     if (key_dtype == ZSB_KEY_I64)
         k_local_moments<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, d_out3,
                                                 (unsigned long long *)d_out_bits2);
@@ -1024,10 +1032,12 @@ int zsb_bucket_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const
     const size_t sm = (size_t)k * 4;
     if (key_dtype == ZSB_KEY_I64) {
         smem_optin(k_bucket_hist<0>, sm);
+        count_launches(1);
         k_bucket_hist<0><<<grid, NT, sm, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
                                                (int)k, (unsigned long long *)d_counts);
     } else {
         smem_optin(k_bucket_hist<1>, sm);
+        count_launches(1);
         k_bucket_hist<1><<<grid, NT, sm, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
                                                (int)k, (unsigned long long *)d_counts);
     }
@@ -1041,10 +1051,12 @@ int zsb_bucket_minmax(const void *d_keys, int32_t key_dtype, int64_t n, const do
     if (rc) return rc;
     if (nb < 0 || nb > 32 || !params) return fail(ZSB_ERR_ARG, "need 0 <= nb <= 32 and params");
     cudaStream_t st = (cudaStream_t)stream;
+    count_launches(1);
     k_minmax_init<<<1, 32, 0, st>>>(nb, (unsigned long long *)d_omin, (unsigned long long *)d_omax);
     ZSB_LAUNCH("k_minmax_init");
     if (n == 0 || nb == 0) return ZSB_OK;
     const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    count_launches(1);
     if (key_dtype == ZSB_KEY_I64)
         k_bucket_minmax<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2],
                                                 params[3], (int)k, nb, d_buckets, (unsigned long long *)d_omin,
@@ -1067,6 +1079,7 @@ int zsb_range_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const 
     ZSB_CUDA(cudaMemsetAsync(d_counts, 0, (size_t)nq * nbins * 8, st));
     if (n == 0 || nq == 0) return ZSB_OK;
     const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    count_launches(1);
     if (key_dtype == ZSB_KEY_I64)
         k_range_hist<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
                                              (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
@@ -1130,6 +1143,7 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ctx.B.cdf = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
+    count_launches(1);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, nparts, ctx.P.tile_len, ctx.P.ntiles, 0, 0.0, 1.0,
                                        0.0, 1.0, MODE_DEST);
     ZSB_LAUNCH("k_init_level1");
