@@ -1827,6 +1827,11 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     if (ZSB_FIN_S2 && (1 << sbits) < 2 * m && sbits < FIN_SBITS_MAX) sbits++;  // S >= 2m when it fits
     const int S = 1 << sbits;
     const uint64_t range = omax - omin;
+    // When (ord - min) leaves 14 free bits, the placed image is packed as
+    // (ord - min) << 14 | record index: one 64-bit compare then orders by
+    // (key, index), and the index needs no separate shared array.
+    constexpr int IB = 14;  // cap <= 16384
+    const bool packed = bitlen64(range) + IB <= 64;
     const bool direct = range < (uint64_t)S;  // one key value per digit
     // d = ((ord - min) >> sh) * M >> 32 with the shifted range below 2^32:
     // monotone in the key and < S; 32-bit multiply only
@@ -1944,8 +1949,13 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         if (d != 0xFFFF && (nb == 0 || !((bigmask[d >> 5] >> (d & 31)) & 1u))) {
             const uint32_t old = atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
             const uint32_t pos = (old >> (16 * (d & 1))) & 0xFFFFu;
-            Bo[pos] = o[j];
-            Ix[pos] = (uint16_t)(base + j * 32);
+            const uint32_t ri = (uint32_t)(base + j * 32);
+            if (packed) {
+                Bo[pos] = ((o[j] - omin) << IB) | ri;
+            } else {
+                Bo[pos] = o[j];
+                Ix[pos] = (uint16_t)ri;
+            }
         }
     }
     if (nb > 0) {
@@ -2010,8 +2020,13 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             b0 = __shfl_sync(0xffffffffu, b0, leader);
             if (sl >= 0) {
                 const uint32_t pos = b0 + __popc(peers & lt);
-                Bo[pos] = o[j];
-                Ix[pos] = (uint16_t)(base + j * 32);
+                const uint32_t ri = (uint32_t)(base + j * 32);
+                if (packed) {
+                    Bo[pos] = ((o[j] - omin) << IB) | ri;
+                } else {
+                    Bo[pos] = o[j];
+                    Ix[pos] = (uint16_t)ri;
+                }
             }
         }
     }
@@ -2020,8 +2035,9 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     // ---- rank inside each sub-bucket by (key, record index) and store to
     //      the final position; ties keep input order (stable)
     for (int i = tid; i < m; i += FT) {
-        const uint64_t ov = Bo[i];
-        const int idx = Ix[i];
+        const uint64_t pv = Bo[i];
+        const uint64_t ov = packed ? (pv >> IB) + omin : pv;
+        const int idx = packed ? (int)(pv & ((1u << IB) - 1)) : (int)Ix[i];
         const int d = digit(ov);
         const int a = d ? (int)((const uint16_t *)cw)[d - 1] : 0, z = ((const uint16_t *)cw)[d];
         const int c = z - a;
@@ -2031,7 +2047,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
                 rank = 0;
                 for (int x = a; x < z; x++) {
                     const uint64_t ox = Bo[x];
-                    rank += (ox < ov) || (ox == ov && Ix[x] < idx);
+                    rank += packed ? (ox < pv) : ((ox < ov) || (ox == ov && Ix[x] < idx));
                 }
             }
         } else if (i == a) {  // oversized sub-bucket, placed stably: refine unless already ordered
