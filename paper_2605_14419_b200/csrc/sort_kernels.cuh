@@ -1853,7 +1853,13 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
 #ifndef ZSB_FIN_VDIG
 #define ZSB_FIN_VDIG 1
 #endif
-        vdig = ZSB_FIN_VDIG && isfinite(lo) && isfinite(hi) && span > 0.0 && isfinite(span) && isfinite(vinv) && !direct;
+        // inside one sign and at most two adjacent binades the ordered image is
+        // linear in the value to within 2x: keep the cheaper integer digit there
+        const uint64_t blo = key_from_ord<KK>(omin), bhi = key_from_ord<KK>(omax);
+        const int elo = (int)((blo >> 52) & 0x7FF), ehi = (int)((bhi >> 52) & 0x7FF);
+        const bool linear = ((blo ^ bhi) >> 63) == 0 && abs(ehi - elo) <= 1;
+        vdig = ZSB_FIN_VDIG && !linear && isfinite(lo) && isfinite(hi) && span > 0.0 && isfinite(span) &&
+               isfinite(vinv) && !direct;
         vlo = lo;
     }
     auto digit = [&](uint64_t ov) -> int {
