@@ -1754,6 +1754,16 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     const uint64_t *kin = nullptr;
     const P *pin = nullptr;
     stage_run<P, PB>(smem + L.off_o, sk, smem + L.off_pb, sp, m, bar, kin, pin);
+    // sub-bucket count S depends on m only: clear the counters while the copies land
+    int sbits = 5;
+    while ((1 << sbits) < m && sbits < FIN_SBITS_MAX) sbits++;
+#ifndef ZSB_FIN_S2
+#define ZSB_FIN_S2 1
+#endif
+    if (ZSB_FIN_S2 && (1 << sbits) < 2 * m && sbits < FIN_SBITS_MAX) sbits++;  // S >= 2m when it fits
+    const int S = 1 << sbits;
+    for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
+    for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
     mbar_wait(bar, parity);
     parity ^= 1u;
     __syncthreads();
@@ -1819,13 +1829,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         }
         return;
     }
-    int sbits = 5;
-    while ((1 << sbits) < m && sbits < FIN_SBITS_MAX) sbits++;
-#ifndef ZSB_FIN_S2
-#define ZSB_FIN_S2 1
-#endif
-    if (ZSB_FIN_S2 && (1 << sbits) < 2 * m && sbits < FIN_SBITS_MAX) sbits++;  // S >= 2m when it fits
-    const int S = 1 << sbits;
     const uint64_t range = omax - omin;
     // When (ord - min) leaves 14 free bits, the placed image is packed as
     // (ord - min) << 14 | record index: one 64-bit compare then orders by
@@ -1844,12 +1847,10 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     // positive constant keep the digit monotone in the key.
     bool vdig = false;
     double vlo = 0.0, vinv = 0.0;
-    __shared__ double s_vinv;
     if constexpr (KK == KEY_F64) {
         const double lo = key_value<KK>(key_from_ord<KK>(omin)), hi = key_value<KK>(key_from_ord<KK>(omax));
         const double span = __dsub_rn(hi, lo);
-        if (tid == 0) s_vinv = (double)S / span;  // one fp64 division, read after the barrier below
-        vinv = 1.0;
+        vinv = (double)S * __drcp_rn(span);  // any positive scale keeps the digit monotone (clamped to S - 1)
 #ifndef ZSB_FIN_VDIG
 #define ZSB_FIN_VDIG 1
 #endif
@@ -1870,13 +1871,6 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         const uint64_t x = ov - omin;
         return direct ? (int)x : (int)__umulhi((uint32_t)(x >> sh), M);
     };
-    for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
-    for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
-    __syncthreads();
-    if constexpr (KK == KEY_F64) {
-        vinv = s_vinv;
-        vdig = vdig && isfinite(vinv);
-    }
     FIN_MARK(2);
     // ---- histogram (16-bit counters: no carry, counts <= cap < 2^16)
     uint32_t dpk[(F + 1) / 2];  // digits, two per register
