@@ -212,10 +212,12 @@ __device__ __forceinline__ int32_t bucket_cdf(double x, const SegParams &p, cons
     return bi < p.k ? bi : p.k - 1;
 }
 
-template <int KK>
+// BM = 1: the caller guarantees MODE_ZCDF (the level-1 kernels dispatch on the
+// mode once per CTA, so the hot loop carries one mapping, not four).
+template <int KK, int BM = 0>
 __device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p, int64_t pos = 0,
                                               const DestCuts *cuts = nullptr, const float2 *cdf = nullptr) {
-    if (p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
+    if (BM == 1 || p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
     if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
     if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
     if (p.mode == MODE_DEST) return dest_of<KK>(bits, pos, cuts);

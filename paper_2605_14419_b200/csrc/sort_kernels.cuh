@@ -667,10 +667,10 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
     __syncthreads();
 }
 
-template <int KK, int PB, int SW>
-__global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
-                                                              int nseg, const uint32_t *__restrict__ mat,
-                                                              int dst_sel, long long *prof, int tie_check) {
+template <int KK, int PB, int SW, int BM>
+__device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *__restrict__ segs, int nseg,
+                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof,
+                                             int tie_check) {
 #ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
     long long t_mark = prof ? clock64() : 0;
     long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
@@ -767,7 +767,8 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         uint32_t pk[ITEMS];  // bucket | rank << 16
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const int bkj = (base + j * 32 < nvalid) ? seg_bucket<KK>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
+            const int bkj =
+                (base + j * 32 < nvalid) ? seg_bucket<KK, BM>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
             uint32_t old = 0, after = 0;
             const int q = w * k + (bkj < 0 ? 0 : bkj);
             const uint32_t sh = 16 * (q & 1);
@@ -839,6 +840,16 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         for (int q = 0; q < 6; q++) prof[(int64_t)blockIdx.x * 8 + q] = acc_ph[q];
 #endif
 #undef SCAT_MARK
+}
+
+template <int KK, int PB, int SW>
+__global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
+                                                              int nseg, const uint32_t *__restrict__ mat,
+                                                              int dst_sel, long long *prof, int tie_check) {
+    if (segs[find_seg(segs, nseg, blockIdx.x)].mode == MODE_ZCDF)
+        scatter_body<KK, PB, SW, 1>(B, segs, nseg, mat, dst_sel, prof, tie_check);
+    else
+        scatter_body<KK, PB, SW, 0>(B, segs, nseg, mat, dst_sel, prof, tie_check);
 }
 
 // Probe (once per device, at first use): do the lanes of one warp that hit
