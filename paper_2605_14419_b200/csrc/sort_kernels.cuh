@@ -401,11 +401,11 @@ __host__ __device__ inline size_t hist_smem(int kmax, bool ring) {
     return o;
 }
 
-template <int KK>
-__global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                             uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok,
-                                             unsigned long long *scan_status, int scan_words,
-                                             unsigned long long *ctrl) {
+template <int KK, int BM>
+__device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__restrict__ segs, int nseg,
+                                          uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok,
+                                          unsigned long long *scan_status, int scan_words,
+                                          unsigned long long *ctrl) {
     extern __shared__ __align__(128) uint32_t hist[];
     __shared__ uint64_t full[HIST_STAGES];
     if (blockIdx.x == 0 && ctrl) {  // state of the kernels that follow (saves separate memsets)
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restr
     bool nan = false;
     auto count = [&](uint64_t b, int64_t i) {
         if (screen) nan |= __longlong_as_double((long long)b) != __longlong_as_double((long long)b);
-        atomicAdd(&hist[seg_bucket<KK>(b, p, i, B.cuts, cdf)], 1u);
+        atomicAdd(&hist[seg_bucket<KK, BM>(b, p, i, B.cuts, cdf)], 1u);
     };
     const uint64_t *tsrc = src + t0;
     const int64_t len = t1 - t0;
@@ -484,6 +484,17 @@ __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restr
     }
     if (__syncthreads_or(nan) && threadIdx.x == 0) *status = 3;  // ZSB_ERR_NAN
     for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
+}
+
+template <int KK>
+__global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
+                                             uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok,
+                                             unsigned long long *scan_status, int scan_words,
+                                             unsigned long long *ctrl) {
+    if (segs[find_seg(segs, nseg, blockIdx.x)].mode == MODE_ZCDF)
+        hist_body<KK, 1>(B, segs, nseg, mat, status, stage_ok, scan_status, scan_words, ctrl);
+    else
+        hist_body<KK, 0>(B, segs, nseg, mat, status, stage_ok, scan_status, scan_words, ctrl);
 }
 
 // ------------------------------------------------------------------- K3
