@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <type_traits>
 namespace cg = cooperative_groups;
 
 #include "common.cuh"
@@ -1885,24 +1886,34 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
                isfinite(vinv) && !direct;
         vlo = lo;
     }
-    auto digit = [&](uint64_t ov) -> int {
-        if (KK == KEY_F64 && vdig) {
+    // digit of an ordered image; VD = value-space (float64 runs spanning
+    // binades), else the integer map (`direct` folds into M = 2^32 with sh = 0)
+    auto digit_t = [&](auto vd_t, uint64_t ov) -> int {
+        if constexpr (decltype(vd_t)::value) {
             const int d = (int)__dmul_rn(__dsub_rn(key_value<KK>(key_from_ord<KK>(ov)), vlo), vinv);
             return d < S ? d : S - 1;
+        } else {
+            const uint64_t x = ov - omin;
+            return direct ? (int)x : (int)__umulhi((uint32_t)(x >> sh), M);
         }
-        const uint64_t x = ov - omin;
-        return direct ? (int)x : (int)__umulhi((uint32_t)(x >> sh), M);
+    };
+    auto digit = [&](uint64_t ov) -> int {
+        return (KK == KEY_F64 && vdig) ? digit_t(std::true_type{}, ov) : digit_t(std::false_type{}, ov);
     };
     FIN_MARK(2);
     // ---- histogram (16-bit counters: no carry, counts <= cap < 2^16)
     uint32_t dpk[(F + 1) / 2];  // digits, two per register
+    auto hist_t = [&](auto vd_t) {
 #pragma unroll
-    for (int j = 0; j < F; j++) {
-        const int d = (base + j * 32 < m) ? digit(o[j]) : 0xFFFF;
-        if (j & 1) dpk[j >> 1] |= (uint32_t)d << 16;
-        else dpk[j >> 1] = (uint32_t)d;
-        if (d != 0xFFFF) atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
-    }
+        for (int j = 0; j < F; j++) {
+            const int d = (base + j * 32 < m) ? digit_t(vd_t, o[j]) : 0xFFFF;
+            if (j & 1) dpk[j >> 1] |= (uint32_t)d << 16;
+            else dpk[j >> 1] = (uint32_t)d;
+            if (d != 0xFFFF) atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
+        }
+    };
+    if (KK == KEY_F64 && vdig) hist_t(std::true_type{});
+    else hist_t(std::false_type{});
     __syncthreads();
     FIN_MARK(3);
     // ---- exclusive scan of the counters in place (they become the cursors;
@@ -2056,32 +2067,45 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     FIN_MARK(5);
     // ---- rank inside each sub-bucket by (key, record index) and store to
     //      the final position; ties keep input order (stable)
-    for (int i = tid; i < m; i += FT) {
-        const uint64_t pv = Bo[i];
-        const uint64_t ov = packed ? (pv >> IB) + omin : pv;
-        const int idx = packed ? (int)(pv & ((1u << IB) - 1)) : (int)Ix[i];
-        const int d = digit(ov);
-        const int a = d ? (int)((const uint16_t *)cw)[d - 1] : 0, z = ((const uint16_t *)cw)[d];
-        const int c = z - a;
-        int rank = i - a;
-        if (c <= fin_ins) {
-            if (c > 1) {
-                rank = 0;
-                for (int x = a; x < z; x++) {
-                    const uint64_t ox = Bo[x];
-                    rank += packed ? (ox < pv) : ((ox < ov) || (ox == ov && Ix[x] < idx));
+    // (one loop per (packed, digit) combination: the flags are uniform per run)
+    auto rank_t = [&](auto pk_t, auto vd_t) {
+        constexpr bool PK = decltype(pk_t)::value;
+        for (int i = tid; i < m; i += FT) {
+            const uint64_t pv = Bo[i];
+            const uint64_t ov = PK ? (pv >> IB) + omin : pv;
+            const int idx = PK ? (int)(pv & ((1u << IB) - 1)) : (int)Ix[i];
+            const int d = digit_t(vd_t, ov);
+            const int a = d ? (int)((const uint16_t *)cw)[d - 1] : 0, z = ((const uint16_t *)cw)[d];
+            const int c = z - a;
+            int rank = i - a;
+            if (c <= fin_ins) {
+                if (c > 1) {
+                    rank = 0;
+                    for (int x = a; x < z; x++) {
+                        const uint64_t ox = Bo[x];
+                        if constexpr (PK) rank += ox < pv;
+                        else rank += (ox < ov) || (ox == ov && Ix[x] < idx);
+                    }
+                }
+            } else if (i == a) {  // oversized sub-bucket, placed stably: refine unless already ordered
+                bool sorted = true;
+                for (int x = a + 1; x < z && sorted; x++) sorted = Bo[x - 1] <= Bo[x];
+                if (!sorted) {
+                    unsigned long long r = atomicAdd(refine_count, 1ull);
+                    refine[r] = Entry{e.start + a, c, 2};
                 }
             }
-        } else if (i == a) {  // oversized sub-bucket, placed stably: refine unless already ordered
-            bool sorted = true;
-            for (int x = a + 1; x < z && sorted; x++) sorted = Bo[x - 1] <= Bo[x];
-            if (!sorted) {
-                unsigned long long r = atomicAdd(refine_count, 1ull);
-                refine[r] = Entry{e.start + a, c, 2};
-            }
+            ok[a + rank] = key_bits(ov, idx);
+            if constexpr (PB != 0) op[a + rank] = pin[idx];
         }
-        ok[a + rank] = key_bits(ov, idx);
-        if constexpr (PB != 0) op[a + rank] = pin[idx];
+    };
+    const bool vd = KK == KEY_F64 && vdig;
+    if (packed) {
+        if (vd) rank_t(std::true_type{}, std::true_type{});
+        else rank_t(std::true_type{}, std::false_type{});
+    } else {
+        if (vd) rank_t(std::false_type{}, std::true_type{});
+        else rank_t(std::false_type{}, std::false_type{});
     }
     FIN_MARK(6);
 #undef FIN_MARK
