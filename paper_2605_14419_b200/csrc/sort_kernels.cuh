@@ -1976,20 +1976,31 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     const int nb = nbig;  // <= m / (fin_ins + 1) <= FIN_BIG_MAX
     FIN_MARK(4);
     // ---- place (atomic cursors; oversized digits go through the stable path)
+    auto place_t = [&](auto pk_t, auto big_t) {
 #pragma unroll
-    for (int j = 0; j < F; j++) {
-        const int d = (int)((dpk[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
-        if (d != 0xFFFF && (nb == 0 || !((bigmask[d >> 5] >> (d & 31)) & 1u))) {
-            const uint32_t old = atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
-            const uint32_t pos = (old >> (16 * (d & 1))) & 0xFFFFu;
-            const uint32_t ri = (uint32_t)(base + j * 32);
-            if (packed) {
-                Bo[pos] = ((o[j] - omin) << IB) | ri;
-            } else {
-                Bo[pos] = o[j];
-                Ix[pos] = (uint16_t)ri;
+        for (int j = 0; j < F; j++) {
+            const int d = (int)((dpk[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
+            bool go = d != 0xFFFF;
+            if constexpr (decltype(big_t)::value) go = go && !((bigmask[d >> 5] >> (d & 31)) & 1u);
+            if (go) {
+                const uint32_t old = atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
+                const uint32_t pos = (old >> (16 * (d & 1))) & 0xFFFFu;
+                const uint32_t ri = (uint32_t)(base + j * 32);
+                if constexpr (decltype(pk_t)::value) {
+                    Bo[pos] = ((o[j] - omin) << IB) | ri;
+                } else {
+                    Bo[pos] = o[j];
+                    Ix[pos] = (uint16_t)ri;
+                }
             }
         }
+    };
+    if (packed) {
+        if (nb) place_t(std::true_type{}, std::true_type{});
+        else place_t(std::true_type{}, std::false_type{});
+    } else {
+        if (nb) place_t(std::false_type{}, std::true_type{});
+        else place_t(std::false_type{}, std::false_type{});
     }
     if (nb > 0) {
         // Stable placement of the oversized digits: sort their digit list,
