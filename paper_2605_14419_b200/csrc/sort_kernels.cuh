@@ -757,16 +757,18 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         for (int j = 0; j < ITEMS; j++) key[j] = base + j * 32 < nv0 ? __ldcs(sk + t0 + base + j * 32) : 0ull;
     }
     int rb = 0, prev_nvalid = 0;  // counter/run-start set of this round; records staged by the previous round
-    for (int64_t r0 = t0; r0 < t1; r0 += ROUND) {
-        SCAT_MARK(5);
-        const int nvalid = (int)min((int64_t)ROUND, t1 - r0);
+    // FULL: this round and the previous one hold ROUND records (all rounds
+    // but the first and the last): no per-item bounds checks
+    auto round_t = [&](auto full_t, int64_t r0, int nvalid) {
+        constexpr bool FULL = decltype(full_t)::value;
         uint16_t *cnt = cnt2 + rb * NC;
         uint16_t *lst = lst2 + rb * (k + 2);
         const uint16_t *lstp = lst2 + (rb ^ 1) * (k + 2);
         P pay[ITEMS];
         if constexpr (PB != 0) {
 #pragma unroll
-            for (int j = 0; j < ITEMS; j++) pay[j] = base + j * 32 < nvalid ? __ldcs(sp + r0 + base + j * 32) : (P)0;
+            for (int j = 0; j < ITEMS; j++)
+                pay[j] = (FULL || base + j * 32 < nvalid) ? __ldcs(sp + r0 + base + j * 32) : (P)0;
         }
         // phase A: bucket + rank of item j (one shared atomic on its
         // per-(warp, bucket) u16 counter: the returned count is its rank among
@@ -779,8 +781,9 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         uint32_t pk[ITEMS];  // bucket | rank << 16
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const int bkj =
-                (base + j * 32 < nvalid) ? seg_bucket<KK, BM>(key[j], p, r0 + base + j * 32, B.cuts, cdf) : -1;
+            const int bkj = (FULL || base + j * 32 < nvalid)
+                                ? seg_bucket<KK, BM>(key[j], p, r0 + base + j * 32, B.cuts, cdf)
+                                : -1;
             uint32_t old = 0, after = 0;
             const int q = w * k + (bkj < 0 ? 0 : bkj);
             const uint32_t sh = 16 * (q & 1);
@@ -798,7 +801,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             }
             pk[j] = bkj >= 0 ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
             const int i = threadIdx.x + j * ST;
-            if (i < prev_nvalid) {
+            if (FULL || i < prev_nvalid) {
                 const int b = stb[i];
                 const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
                 dk[dst] = stk[i];
@@ -808,7 +811,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         __syncthreads();
         SCAT_MARK(1);  // buckets + counting + previous round's writes
         // phase B: cursors advance past the previous round's runs; scan
-        if (prev_nvalid)
+        if (FULL || prev_nvalid)
             for (int b = threadIdx.x; b < k; b += ST) cur[b] += (uint32_t)(lstp[b + 1] - lstp[b]);
         scan_wd<SW>(cnt, k, lst, wtot);
         SCAT_MARK(2);  // scan
@@ -816,7 +819,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         // counter set for the next round; load the next round's keys
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            if (pk[j] != 0xffffffffu) {
+            if (FULL || pk[j] != 0xffffffffu) {
                 const int b = (int)(pk[j] & 0xFFFFu);
                 const uint32_t pos = (uint32_t)cnt[w * k + b] + (pk[j] >> 16);
                 stk[pos] = key[j];
@@ -834,6 +837,12 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         }
         __syncthreads();
         SCAT_MARK(3);  // placement
+    };
+    for (int64_t r0 = t0; r0 < t1; r0 += ROUND) {
+        SCAT_MARK(5);
+        const int nvalid = (int)min((int64_t)ROUND, t1 - r0);
+        if (nvalid == ROUND && prev_nvalid == ROUND) round_t(std::true_type{}, r0, nvalid);
+        else round_t(std::false_type{}, r0, nvalid);
         prev_nvalid = nvalid;
         rb ^= 1;
     }
