@@ -465,8 +465,17 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
             const int clen = (int)min((int64_t)HIST_CHUNK, len - c0);
             const uint64_t *kb = ring + (size_t)st * HIST_CHUNK;
             const int cfull = clen & ~1;  // an odd last key is outside the 16-byte copy
+            if (clen == HIST_CHUNK) {  // full chunk: fixed trip count, loads first
+                constexpr int PER = HIST_CHUNK / HT;
+                uint64_t kv[PER];
+#pragma unroll
+                for (int u = 0; u < PER; u++) kv[u] = kb[threadIdx.x + u * HT];
+#pragma unroll
+                for (int u = 0; u < PER; u++) count(kv[u], t0 + c0 + threadIdx.x + u * HT);
+            } else {
 #pragma unroll 4
-            for (int i = threadIdx.x; i < cfull; i += HT) count(kb[i], t0 + c0 + i);
+                for (int i = threadIdx.x; i < cfull; i += HT) count(kb[i], t0 + c0 + i);
+            }
             if (clen & 1 && threadIdx.x == 0) count(__ldcs(tsrc + c0 + clen - 1), t0 + c0 + clen - 1);
             __syncthreads();  // stage consumed
             if (threadIdx.x == 0 && c + HIST_STAGES < nch) issue(c + HIST_STAGES);
