@@ -752,6 +752,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
 
     const int w = threadIdx.x >> 5, lane = lane_id();
     const unsigned lt = lanemask_lt();
+    const uint64_t l2pol = l2_evict_last_policy();
     // Pipeline across rounds.  Round r's staged records are written to HBM
     // while round r+1 computes its buckets and counts (phase A), so the store
     // traffic overlaps the arithmetic; counters and run-start tables
@@ -813,8 +814,9 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             if (FULL || i < prev_nvalid) {
                 const int b = stb[i];
                 const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
-                dk[dst] = stk[i];
-                if constexpr (PB != 0) dp[dst] = stp[i];
+                // evict_last: the runs (and the finish's input) stay in L2
+                st_keep(dk + dst, stk[i], l2pol);
+                if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
             }
         }
         __syncthreads();
@@ -860,8 +862,8 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         for (int i = threadIdx.x; i < prev_nvalid; i += ST) {
             const int b = stb[i];
             const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
-            dk[dst] = stk[i];
-            if constexpr (PB != 0) dp[dst] = stp[i];
+            st_keep(dk + dst, stk[i], l2pol);
+            if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
         }
     }
     SCAT_MARK(4);
