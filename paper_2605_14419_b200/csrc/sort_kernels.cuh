@@ -1798,12 +1798,8 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     const P *pin = nullptr;
     stage_run<P, PB>(smem + L.off_o, sk, smem + L.off_pb, sp, m, bar, kin, pin);
     // sub-bucket count S depends on m only: clear the counters while the copies land
-    int sbits = 5;
-    while ((1 << sbits) < m && sbits < FIN_SBITS_MAX) sbits++;
-#ifndef ZSB_FIN_S2
-#define ZSB_FIN_S2 1
-#endif
-    if (ZSB_FIN_S2 && (1 << sbits) < 2 * m && sbits < FIN_SBITS_MAX) sbits++;  // S >= 2m when it fits
+    // S = the smallest power of two >= 2m (>= 32), capped at 2^FIN_SBITS_MAX
+    const int sbits = min(FIN_SBITS_MAX, max(5, 33 - __clz(m > 1 ? m - 1 : 1)));
     const int S = 1 << sbits;
     for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
     for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
