@@ -1522,10 +1522,27 @@ __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, 
     __shared__ long long sh[5][32];
     __shared__ long long carry[5];
     __shared__ int kmax;
+    __shared__ unsigned long long tot_rec;
     if (threadIdx.x < 5) carry[threadIdx.x] = 0;
-    if (threadIdx.x == 0) kmax = 1;
+    if (threadIdx.x == 0) {
+        kmax = 1;
+        tot_rec = 0;
+    }
     __syncthreads();
     (void)NV;
+    // tile length of the level: min_tile, raised (up to 4x) while the level
+    // still yields ~8 tiles per SM -- long recursion levels then run fewer,
+    // longer tiles (more pipelined rounds per CTA), short ones keep parallelism
+    {
+        unsigned long long t = 0;
+        for (int q = threadIdx.x; q < nseg; q += blockDim.x) t += (unsigned long long)segs[q].len;
+        t = warp_sum(t);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&tot_rec, t);
+        __syncthreads();
+        int64_t mt = (int64_t)(tot_rec / (unsigned long long)(148 * 8));
+        mt = mt < min_tile ? min_tile : (mt > 4 * (int64_t)min_tile ? 4 * (int64_t)min_tile : mt);
+        min_tile = (int32_t)((mt + 255) & ~(int64_t)255);
+    }
     for (int base = 0; base < nseg; base += 1024) {
         int s = base + threadIdx.x;
         long long v[5] = {0, 0, 0, 0, 0};

@@ -122,7 +122,7 @@ int num_sms() {
 
 constexpr int K_LEVEL1_MAX = KSCAT_MAX;  // fan-out of one scatter pass
 constexpr int KMAX_CHILD = 1024;
-constexpr int MIN_TILE = 8192;
+constexpr int MIN_TILE = 8192;  // recursion tile floor (k_plan raises it on long levels)
 
 int finish_cap(int pb) { return FT * (pb == 8 ? FinItems<8>::F : (pb == 4 ? FinItems<4>::F : FinItems<0>::F)); }
 
@@ -349,12 +349,15 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
-    const size_t kbytes = hist_smem(kmax, true);
+    // the TMA ring pays off on long tiles (level 1); short recursion tiles run
+    // several CTAs per SM without it
+    const bool ring = segs_level1;
+    const size_t kbytes = hist_smem(kmax, ring);
     smem_optin(k_hist<KK>, kbytes);
     const int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
     {
         PhaseScope ph(PH_HIST, c.st);
-        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, 1, status,
+        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, ring ? 1 : 0, status,
                                                          (int)(sblocks + 1), ctrl);
     }
     ZSB_LAUNCH("k_hist");
