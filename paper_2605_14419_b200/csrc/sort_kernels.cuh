@@ -774,7 +774,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         uint16_t *cnt = cnt2 + rb * NC;
         uint16_t *lst = lst2 + rb * (k + 2);
         const uint16_t *lstp = lst2 + (rb ^ 1) * (k + 2);
-        P pay[ITEMS];
+        P pay[PB != 0 ? ITEMS : 1];
         if constexpr (PB != 0) {
 #pragma unroll
             for (int j = 0; j < ITEMS; j++)
@@ -1027,152 +1027,11 @@ __device__ __forceinline__ int64_t sample_pos(int64_t g, int64_t nitems, int64_t
     return (g < nitems && off < clen) ? (g / SAMP_CHUNK) * stride + off : -1;
 }
 
-template <int KK>
-__global__ void __launch_bounds__(NT) k_sample_moments(const uint64_t *__restrict__ keys, int64_t n,
-                                                       int64_t nchunks, int64_t stride, SampPartial *parts,
-                                                       unsigned long long *ctrl, SegParams *seg, int kf) {
-    const double c0 = key_value<KK>(keys[0]);
-    const int64_t clen = stride < SAMP_CHUNK ? stride : SAMP_CHUNK;
-    const int64_t nitems = nchunks * SAMP_CHUNK, gstride = (int64_t)gridDim.x * NT;
-    unsigned long long omin = ~0ull, omax = 0, nan = 0;
-    double s1 = 0.0, s2 = 0.0, cnt = 0.0;
-    for (int64_t g0 = (int64_t)blockIdx.x * NT + threadIdx.x; g0 < nitems; g0 += SAMP_UNROLL * gstride) {
-        uint64_t b[SAMP_UNROLL];
-        bool v[SAMP_UNROLL];
-#pragma unroll
-        for (int u = 0; u < SAMP_UNROLL; u++) {
-            const int64_t i = sample_pos(g0 + u * gstride, nitems, stride, clen);
-            v[u] = i >= 0;
-            b[u] = v[u] ? __ldcs(keys + i) : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < SAMP_UNROLL; u++) {
-            if (!v[u]) continue;
-            const double x = key_value<KK>(b[u]);
-            if (KK == KEY_F64 && x != x) {
-                nan++;
-                continue;
-            }
-            const uint64_t o = ord_key<KK>(b[u]);
-            omin = o < omin ? o : omin;
-            omax = o > omax ? o : omax;
-            const double d = x - c0;
-            s1 += d;
-            s2 += d * d;
-            cnt += 1.0;
-        }
-    }
-    __shared__ SampPartial wp[NWARPS];
-    __shared__ bool last;
-    const int w = threadIdx.x >> 5, lane = lane_id();
-    auto block_reduce = [&]() {  // warp shuffles, then warp 0 over the warp partials
-        omin = warp_min_u64(omin);
-        omax = warp_max_u64(omax);
-        nan = warp_sum(nan);
-        s1 = warp_sum(s1);
-        s2 = warp_sum(s2);
-        cnt = warp_sum(cnt);
-        if (lane == 0) wp[w] = SampPartial{omin, omax, nan, 0, s1, s2, cnt, 0.0};
-        __syncthreads();
-        if (w == 0) {
-            SampPartial a = lane < NWARPS ? wp[lane] : SampPartial{~0ull, 0, 0, 0, 0.0, 0.0, 0.0, 0.0};
-            omin = warp_min_u64(a.omin);
-            omax = warp_max_u64(a.omax);
-            nan = warp_sum(a.nan);
-            s1 = warp_sum(a.s1);
-            s2 = warp_sum(a.s2);
-            cnt = warp_sum(a.cnt);
-        }
-    };
-    block_reduce();
-    if (threadIdx.x == 0) {
-        parts[blockIdx.x] = SampPartial{omin, omax, nan, 0, s1, s2, cnt, 0.0};
-        __threadfence();
-        last = atomicAdd(&ctrl[C_SAMP_TICKET], 1ull) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    omin = ~0ull, omax = 0, nan = 0, s1 = 0.0, s2 = 0.0, cnt = 0.0;
-    for (int j = threadIdx.x; j < (int)gridDim.x; j += NT) {
-        const unsigned long long qmin = __ldcg(&parts[j].omin), qmax = __ldcg(&parts[j].omax);
-        omin = qmin < omin ? qmin : omin;
-        omax = qmax > omax ? qmax : omax;
-        nan += __ldcg(&parts[j].nan);
-        s1 += __ldcg(&parts[j].s1);
-        s2 += __ldcg(&parts[j].s2);
-        cnt += __ldcg(&parts[j].cnt);
-    }
-    __syncthreads();  // wp reuse
-    block_reduce();
-    if (threadIdx.x != 0) return;
-    ctrl[C_SAMP_TICKET] = 0;
-    ctrl[C_SAMPLE_OK] = 0;
-    if (nan || cnt < 2.0 || omin == omax) return;  // exact K1 decides (NaN status, copy, integer)
-    const double mean = c0 + s1 / cnt;
-    const double dm = mean - c0;
-    double m2 = s2 - 2.0 * dm * s1 + cnt * dm * dm;
-    if (m2 < 0.0) m2 = 0.0;
-    const double sd = sqrt(m2 / cnt);
-    const double vmin = key_value<KK>(key_from_ord<KK>(omin)), vmax = key_value<KK>(key_from_ord<KK>(omax));
-    const double span = (vmax - vmin) / sd;
-    if (!(sd > 0.0) || !isfinite(sd) || !(span > 0.0) || !isfinite(span)) return;
-    SegParams p = *seg;
-    p.center = mean;
-    p.std = sd;
-    p.zmin = (mean - vmin) / sd;
-    p.scale = ((double)p.k * (1.0 - 0x1p-20)) / span;
-    float za, zb;
-    if (!isfinite(p.zmin) || !(p.scale > 0.0) || !isfinite(p.scale) || !zc_coeffs(p, kf, za, zb)) return;
-    p.za = za;
-    p.zb = zb;
-    *seg = p;
-    ctrl[C_SAMPLE_OK] = 1;
-}
-
-template <int KK>
-__global__ void __launch_bounds__(NT) k_sample_cdf(const uint64_t *__restrict__ keys, int64_t n, int64_t nchunks,
-                                                   int64_t stride, unsigned int *fine, unsigned long long *ctrl,
-                                                   SegParams *seg, int kf, float2 *cdf) {
-    if (!ctrl[C_SAMPLE_OK]) return;
-    __shared__ uint32_t fh[KF_MAX];
-    __shared__ bool last;
-    const SegParams p = *seg;
-    const int64_t clen = stride < SAMP_CHUNK ? stride : SAMP_CHUNK;
-    const int64_t nitems = nchunks * SAMP_CHUNK, gstride = (int64_t)gridDim.x * NT;
-    for (int b = threadIdx.x; b < kf; b += NT) fh[b] = 0;
-    __syncthreads();
-    for (int64_t g0 = (int64_t)blockIdx.x * NT + threadIdx.x; g0 < nitems; g0 += SAMP_UNROLL * gstride) {
-        uint64_t b[SAMP_UNROLL];
-        bool v[SAMP_UNROLL];
-#pragma unroll
-        for (int u = 0; u < SAMP_UNROLL; u++) {
-            const int64_t i = sample_pos(g0 + u * gstride, nitems, stride, clen);
-            v[u] = i >= 0;
-            b[u] = v[u] ? __ldcs(keys + i) : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < SAMP_UNROLL; u++)
-            if (v[u]) atomicAdd(&fh[zc_bin(zc_coord(key_value<KK>(b[u]), p.center, p.za, p.zb), kf)], 1u);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kf; b += NT)
-        if (fh[b]) atomicAdd(&fine[b], fh[b]);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&ctrl[C_SAMP_TICKET], 1ull) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (threadIdx.x == 0) ctrl[C_SAMP_TICKET] = 0;
-    build_cdf_block<NT>(fine, kf, nchunks * clen, seg, p, p.za, p.zb, cdf);  // no NaN in the sample
-}
-
 // ------------------------------------------------ fused level-1 mapping
 // One cooperative launch (one CTA per SM, grid barriers between phases)
 // replaces the level-1 chain init -> sample moments -> sample CDF -> exact
 // K1 -> exact fine histogram -> CDF, which cost a launch gap each:
-//   S1  stratified sample moments (as k_sample_moments); every CTA reduces the
+//   S1  stratified sample moments; every CTA reduces the
 //       partials itself, in the same order, so all derive identical params;
 //   S2  sample coarse-bin histogram -> CDF knots (CTA 0), mode MODE_ZCDF;
 // and, only when the sample is degenerate (NaN, all equal, no spread):
