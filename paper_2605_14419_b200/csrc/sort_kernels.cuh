@@ -1287,6 +1287,23 @@ __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64
     return lo;
 }
 
+// A value whose equalised bucket is b (approximately its middle): the knot
+// pair bracketing b + 0.5, linear inside the coarse bin, back through the
+// coarse coordinate.
+__device__ inline double zcdf_inverse(const SegParams &p, const float2 *cdf, int b) {
+    const float t = (float)b + 0.5f;
+    int lo = 0, hi = p.kf - 1;  // first bin whose upper knot exceeds t
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cdf[mid].y <= t) lo = mid + 1;
+        else hi = mid;
+    }
+    const float2 az = cdf[lo];
+    float fr = az.y > az.x ? (t - az.x) / (az.y - az.x) : 0.5f;
+    fr = fminf(fmaxf(fr, 0.0f), 1.0f);
+    return p.center + ((double)lo + (double)fr - (double)p.zb) / (double)p.za;
+}
+
 __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restrict__ segs, int nseg,
                                             const int64_t *__restrict__ kfirst, const uint32_t *__restrict__ mat,
                                             int64_t *__restrict__ bstart, SegParams *children, SegAcc *acc,
@@ -1319,10 +1336,11 @@ __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restri
         atomicAdd(&ctrl[C_ST_FALLBACKS], 1ull);
     } else if (p.mode == MODE_ZCDF) {
         // an equal-population bucket is not a z-interval: centre the child on
-        // one of its own keys (the first record the scatter placed there)
+        // the inverse of the equalised map at the bucket's middle (any value
+        // in or near the bucket conditions the child's moments; it needs no
+        // scattered data, so classify can run beside the scatter)
         ch.mode = MODE_ZSCORE;
-        const uint64_t kb = src_keys(B, ch.src)[st];
-        ch.center = key_kind ? __longlong_as_double((long long)kb) : __ll2double_rn((long long)kb);
+        ch.center = zcdf_inverse(p, B.cdf, b);
     } else {
         ch.mode = MODE_ZSCORE;
         ch.center = __dadd_rn(__dmul_rn(__dsub_rn(__ddiv_rn((double)b + 0.5, p.scale), p.zmin), p.std), p.center);

@@ -345,7 +345,7 @@ int scatter_tie_check() {
 
 template <int KK, int PB>
 int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
-                     bool segs_level1 = false) {
+                     bool segs_level1 = false, cudaEvent_t after_scan = nullptr) {
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
@@ -366,6 +366,7 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
         k_scan<<<(unsigned)sblocks, NT, 0, c.st>>>(mat, mat_entries, status, ctrl);
     }
     ZSB_LAUNCH("k_scan");
+    if (after_scan) ZSB_CUDA(cudaEventRecord(after_scan, c.st));
     const size_t cdf_bytes = (c.B.cdf && segs_level1) ? (size_t)(CDF_KNOTS + 1) * 8 : 0;
     const bool sw16 = scat_warps(kmax, env_int("ZSB_SW16_ABOVE", 512)) == 16 &&
                       scat_layout(kmax, PB, 16).total + cdf_bytes <= (size_t)227 * 1024 - 1024;
@@ -453,7 +454,9 @@ int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev
 // Pinned host mirror of the control block and the level event (per host thread).
 struct HostSync {
     unsigned long long *ctrl = nullptr;
-    cudaEvent_t ev = nullptr;
+    cudaEvent_t ev = nullptr;       // classify done (control block copied)
+    cudaEvent_t ev_scan = nullptr;  // level scan done: classify may start
+    cudaStream_t side = nullptr;    // classify runs here, beside the scatter
     int dev = -1;
 };
 thread_local HostSync g_hs;
@@ -464,7 +467,11 @@ int host_sync_init() {
     if (g_hs.ctrl && g_hs.dev == dev) return ZSB_OK;
     if (!g_hs.ctrl) ZSB_CUDA(cudaHostAlloc((void **)&g_hs.ctrl, C_SLOTS * 8, cudaHostAllocDefault));
     if (g_hs.ev) cudaEventDestroy(g_hs.ev);
+    if (g_hs.ev_scan) cudaEventDestroy(g_hs.ev_scan);
+    if (g_hs.side) cudaStreamDestroy(g_hs.side);
     ZSB_CUDA(cudaEventCreateWithFlags(&g_hs.ev, cudaEventDisableTiming));
+    ZSB_CUDA(cudaEventCreateWithFlags(&g_hs.ev_scan, cudaEventDisableTiming));
+    ZSB_CUDA(cudaStreamCreateWithFlags(&g_hs.side, cudaStreamNonBlocking));
     g_hs.dev = dev;
     return ZSB_OK;
 }
@@ -603,10 +610,15 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             ZSB_LAUNCH("k_seg_moments/params");
         }
         const int dst_sel = (level == 1) ? 1 : ((level % 2 == 0) ? 2 : 1);
-        int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel, level == 1);
+        int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel, level == 1,
+                                          g_hs.ev_scan);
         if (rc) return rc;
-        {  // (C_NCHILD / C_NENTRY were cleared by K2)
-            PhaseScope ph(PH_CLASSIFY, c.st);
+        // classify needs the scanned counts, not the scattered records: it runs
+        // on the side stream while the scatter runs (C_NCHILD / C_NENTRY were
+        // cleared by K2)
+        ZSB_CUDA(cudaStreamWaitEvent(g_hs.side, g_hs.ev_scan, 0));
+        {
+            PhaseScope ph(PH_CLASSIFY, g_hs.side);
             const int64_t need = std::max<int64_t>(1, (std::max(total_slots, total_windows) + 1023) / 1024);
             const int cgrid = (int)std::min<int64_t>(need, (int64_t)num_sms());
             int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = MIN_TILE;
@@ -615,14 +627,15 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             unsigned long long *ref_zero = ctrl + REF_SLOT[2 * par];
             void *args[] = {&seg_cur, &nseg_, &kfirst, &wfirst, &mat, &bstart, &seg_next, &acc, &entries, &ctrl,
                             &cc, &ts, &tw, &Bv, &key_kind, &kmc, &mt, &ref_zero};
-            ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_classify, dim3(cgrid), dim3(1024), args, 0, c.st));
+            ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_classify, dim3(cgrid), dim3(1024), args, 0, g_hs.side));
         }
         ZSB_LAUNCH("k_classify");
         // The host needs this level's outcome (children, sizes of the next
         // level); the finish of this level does not: it is enqueued before the
         // host waits (count on the device), so the GPU goes straight on.
-        ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, c.st));
-        ZSB_CUDA(cudaEventRecord(g_hs.ev, c.st));
+        ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, g_hs.side));
+        ZSB_CUDA(cudaEventRecord(g_hs.ev, g_hs.side));
+        ZSB_CUDA(cudaStreamWaitEvent(c.st, g_hs.ev, 0));  // the finish (and every later level) after classify
         rc = enqueue_finish(entries, ctrl + C_NENTRY, c.L.ent_cap, c.L.ent_cap, par, true);
         if (rc) return rc;
         ZSB_CUDA(cudaEventSynchronize(g_hs.ev));
