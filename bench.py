@@ -52,10 +52,10 @@ def peaks():
 
 def make_workload(cfg: int, rank: int = 0, world: int = 1):
     """Host arrays (keys, payload) for one rank."""
-    from oracle import oracle as O
+    from paper_2605_14419_b200 import datagen
 
     if cfg in (1, 2, 3, 4):
-        return O.make_config(cfg)
+        return datagen.baseline_config(cfg)
     if cfg == 9:
         keys = np.random.default_rng(9).integers(-(2**63), 2**63 - 1, size=10**9, endpoint=True, dtype=np.int64)
         return keys, np.arange(keys.size, dtype=np.int32)

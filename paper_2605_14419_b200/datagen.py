@@ -1,4 +1,5 @@
-"""Counter-based synthetic inputs for BASELINE config 5.
+"""Synthetic inputs: BASELINE configs 1-4 (numpy recipes) and config 5
+(counter-based, on the device) -- SURVEY.md §8(d).
 
 Config 5 is n = 2^31 int64 keys uniform over the full int64 range with 10%
 of positions overwritten by one repeated value, sharded evenly over the
@@ -57,3 +58,72 @@ def config5_keys(offset: int, count: int, n_total: int, device="cuda", chunk: in
         out[s:e] = k
         del i, k, u
     return out
+
+
+# ---------------------------------------------------------------- configs 1-4
+# Host recipes of BASELINE configs 1-4: numpy default_rng,
+# identical arrays to the committed input digests (tests/golden/golden.json,
+# checked in tests/test_datagen.py against the oracle's copy of the recipes).
+
+def baseline_config(index: int, n: int | None = None):
+    """(keys, payload) numpy arrays of BASELINE config ``index`` in 1..4; ``n``
+    overrides the size (same recipe) for scaled-down variants."""
+    import numpy as np
+
+    i64min, i64max = -(2**63), 2**63 - 1
+    if index == 1:  # 10^6 int64 uniform over the full range, seed 0
+        n = n or 10**6
+        keys = np.random.default_rng(0).integers(i64min, i64max, size=n, endpoint=True, dtype=np.int64)
+    elif index == 2:  # 10^7 float64 N(0,1), seed 1
+        n = n or 10**7
+        keys = np.random.default_rng(1).standard_normal(n)
+    elif index == 3:  # 10^7 int64 from 1000 distinct values in [0, 2^40), seed 2
+        n = n or 10**7
+        r = np.random.default_rng(2)
+        while True:
+            vals = r.integers(0, 2**40, 1000, dtype=np.int64)
+            if np.unique(vals).size == 1000:
+                break
+        keys = vals[r.integers(0, 1000, n)]
+    elif index == 4:  # 10^8 float64 lognormal(0, 2) half + sorted half with 1% index-pair swaps, seed 3
+        n = n or 10**8
+        r = np.random.default_rng(3)
+        h = n // 2
+        first = r.lognormal(0.0, 2.0, h)
+        second = np.sort(r.lognormal(0.0, 2.0, n - h))
+        pairs = r.integers(0, n - h, size=(int(0.01 * (n - h)), 2))
+        second = _swap_pairs(second, pairs)
+        keys = np.concatenate([first, second])
+    else:
+        raise ValueError("configs 1..4 are host recipes; config 5 is config5_keys")
+    return np.ascontiguousarray(keys), np.arange(keys.size, dtype=np.int32)
+
+
+def _swap_pairs(arr, pairs):
+    """Apply the index swaps in order (later pairs see earlier swaps), on the
+    device: pairs are processed in rounds of mutually disjoint positions, each
+    round a vectorised exchange."""
+    import numpy as np
+
+    a = torch.from_numpy(np.ascontiguousarray(arr).copy())
+    p = torch.from_numpy(np.ascontiguousarray(pairs.astype(np.int64)))
+    dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    a, p = a.to(dev), p.to(dev)
+    start, m = 0, p.shape[0]
+    while start < m:
+        # longest prefix of the remaining pairs whose positions are all distinct
+        chunk = p[start:start + 8192]
+        flat = chunk.reshape(-1)
+        order = torch.argsort(flat, stable=True)
+        sf = flat[order]
+        dup = torch.zeros_like(flat, dtype=torch.bool)
+        dup[order[1:]] = sf[1:] == sf[:-1]
+        first_conflict = torch.nonzero(dup.reshape(-1, 2).any(dim=1))
+        take = int(first_conflict[0]) if first_conflict.numel() else chunk.shape[0]
+        take = max(take, 1)
+        sel = chunk[:take]
+        i, j = sel[:, 0], sel[:, 1]
+        ai, aj = a[i].clone(), a[j].clone()
+        a[i], a[j] = aj, ai
+        start += take
+    return a.cpu().numpy()
