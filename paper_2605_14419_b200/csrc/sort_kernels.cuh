@@ -1079,6 +1079,8 @@ __global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ 
         const int64_t clen = stride < SAMP_CHUNK ? stride : SAMP_CHUNK;
         const int64_t nitems = nchunks * SAMP_CHUNK;
         SampPartial a{~0ull, 0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+        uint64_t kb0[SAMP_UNROLL];  // the first batch stays in registers for S2
+        bool kv0[SAMP_UNROLL];
         for (int64_t gb = g0; gb < nitems; gb += SAMP_UNROLL * G) {
             uint64_t b[SAMP_UNROLL];
             bool v[SAMP_UNROLL];
@@ -1087,6 +1089,10 @@ __global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ 
                 const int64_t i = sample_pos(gb + u * G, nitems, stride, clen);
                 v[u] = i >= 0;
                 b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+                if (gb == g0) {
+                    kb0[u] = b[u];
+                    kv0[u] = v[u];
+                }
             }
 #pragma unroll
             for (int u = 0; u < SAMP_UNROLL; u++) {
@@ -1159,9 +1165,14 @@ __global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ 
                 bool v[SAMP_UNROLL];
 #pragma unroll
                 for (int u = 0; u < SAMP_UNROLL; u++) {
-                    const int64_t i = sample_pos(gb + u * G, nitems, stride, clen);
-                    v[u] = i >= 0;
-                    b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+                    if (gb == g0) {  // still in registers from S1
+                        b[u] = kb0[u];
+                        v[u] = kv0[u];
+                    } else {
+                        const int64_t i = sample_pos(gb + u * G, nitems, stride, clen);
+                        v[u] = i >= 0;
+                        b[u] = v[u] ? __ldcs(keys + i) : 0ull;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < SAMP_UNROLL; u++)
