@@ -306,6 +306,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// L2 prefetch of a 16-byte-aligned range (size a multiple of 16) by the copy
+// engine: no registers, no shared memory, no completion to wait for.
+__device__ __forceinline__ void prefetch_l2_bulk(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Stores with an L2 evict_last policy (the scatter's runs: its output is the
 // finish's input, and keeping it in L2 saves both DRAM write-back and the
 // finish's re-read; measured 10 us on C2).

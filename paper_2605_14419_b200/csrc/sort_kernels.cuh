@@ -1390,7 +1390,7 @@ __device__ __forceinline__ int window_item(int64_t g, const SegParams *__restric
     const int64_t last = bs[b1] - bs[b1 - 1];
     int64_t e0 = bs[b0], e1 = bs[b1];
     int ne = 0;
-    if (last > cc.half) {
+    if (last > cc.cap - cc.half) {
         e1 = bs[b1 - 1];
         if (last <= cc.cap) e[ne++] = Entry{bs[b1 - 1], (int32_t)last, dst};  // a mid-size bucket is a run of its own
     }
@@ -1627,10 +1627,12 @@ __device__ __forceinline__ StageSpan stage_span(const void *src, int m, int esz)
                      bulk ? (int)((A16 - A) / esz) : m, bulk ? (int)((E16 - A) / esz) : m};
 }
 
-// Stage the keys (and payload) of a finish run into shared memory with one
-// mbarrier phase: thread 0 arms it with the total interior bytes and issues
-// the bulk copies; warps 1 and 2 load the ragged ends.  Callers wait on `bar`
-// and then barrier before reading.
+// Stage the keys (and payload) of a finish run into shared memory: thread 0
+// arms bar[0] with the key bytes and bar[1] with the payload bytes and issues
+// the bulk copies; warps 1 and 2 load the ragged ends.  Callers wait on
+// bar[0] and barrier before reading keys, and on bar[1] (one phase per run,
+// armed even without payload bytes) before reading the payload, which is
+// needed only at the final store: its copy lands while the keys are ranked.
 template <typename P, int PB>
 __device__ __forceinline__ void stage_run(unsigned char *karea, const uint64_t *sk, unsigned char *parea, const P *sp,
                                           int m, uint64_t *bar, const uint64_t *&kst, const P *&pst) {
@@ -1647,10 +1649,11 @@ __device__ __forceinline__ void stage_run(unsigned char *karea, const uint64_t *
     const int tid = threadIdx.x;
     if (tid == 0) {
         fence_proxy_async_smem();
-        mbar_expect_tx(bar, ks.bytes + ps.bytes);
-        if (ks.bytes) bulk_g2s((unsigned char *)kd + (ks.a16 - (uintptr_t)sk), (const void *)ks.a16, ks.bytes, bar);
+        mbar_expect_tx(&bar[0], ks.bytes);
+        mbar_expect_tx(&bar[1], ps.bytes);
+        if (ks.bytes) bulk_g2s((unsigned char *)kd + (ks.a16 - (uintptr_t)sk), (const void *)ks.a16, ks.bytes, &bar[0]);
         if (PB != 0 && ps.bytes)
-            bulk_g2s((unsigned char *)pd + (ps.a16 - (uintptr_t)sp), (const void *)ps.a16, ps.bytes, bar);
+            bulk_g2s((unsigned char *)pd + (ps.a16 - (uintptr_t)sp), (const void *)ps.a16, ps.bytes, &bar[1]);
     } else if (tid >= 32 && tid < 64) {  // key ends
         const int q = tid - 32;
         if (q < ks.h) kd[q] = sk[q];
@@ -1708,8 +1711,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     const int S = 1 << sbits;
     for (int q = tid; q < S / 2; q += FT) cw[q] = 0u;
     for (int q = tid; q < S / 32; q += FT) bigmask[q] = 0u;
-    mbar_wait(bar, parity);
-    parity ^= 1u;
+    mbar_wait(&bar[0], parity);
     __syncthreads();
     FIN_MARK(7);  // staged
 
@@ -1761,6 +1763,8 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         return kb;
     };
     if (omin == omax) {  // all equal: already in stable order
+        mbar_wait(&bar[1], parity);  // payload staged
+        parity ^= 1u;
         if (e.src != 2) {
 #pragma unroll
             for (int j = 0; j < F; j++) {
@@ -1784,7 +1788,11 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     // monotone in the key and < S; 32-bit multiply only
     const int sh = max(0, bitlen64(range) - 32);
     const uint32_t r32 = (uint32_t)(range >> sh);
-    const uint32_t M = direct ? 0u : (uint32_t)((((uint64_t)S) << 32) / ((uint64_t)r32 + 1));
+    // M <= S * 2^32 / (r32 + 1) (division rounded toward zero, then truncated),
+    // so umulhi(x, M) < S for every x <= r32; a 64-bit integer division would
+    // cost every thread ~70 instructions
+    const uint32_t M = direct ? 0u
+                              : (uint32_t)fmin(4294967295.0, __ddiv_rz((double)S * 4294967296.0, (double)r32 + 1.0));
     // float64 keys over a finite range take their digit in value space: the
     // ordered images are exponentially non-uniform near 0 (a run straddling
     // 0 would crowd into a few digits).  Rounded subtraction and product by a
@@ -2031,6 +2039,8 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             if constexpr (PB != 0) op[a + rank] = pin[idx];
         }
     };
+    mbar_wait(&bar[1], parity);  // payload staged (landed while the keys were ranked)
+    parity ^= 1u;
     const bool vd = KK == KEY_F64 && vdig;
     if (packed) {
         if (vd) rank_t(std::true_type{}, std::true_type{});
@@ -2043,30 +2053,59 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
 #undef FIN_MARK
 }
 
+// L2 prefetch of a finish run's keys and payload (aligned interiors).
+template <int PB>
+__device__ __forceinline__ void finish_prefetch(const Buffers &B, const Entry e) {
+    using P = typename PayloadT<PB>::T;
+    if (e.len <= 0) return;
+    const StageSpan ks = stage_span(src_keys(B, e.src) + e.start, e.len, 8);
+    if (ks.bytes) prefetch_l2_bulk((const void *)ks.a16, ks.bytes);
+    if constexpr (PB != 0) {
+        const StageSpan ps = stage_span(src_pay<PB>(B, e.src) + e.start, e.len, PB);
+        if (ps.bytes) prefetch_l2_bulk((const void *)ps.a16, ps.bytes);
+    }
+}
+
 // Persistent finish: the work count is read from device memory (written by
 // the classify or a previous finish), so the host enqueues without a sync.
 template <int KK, int PB>
 __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
                                                   const unsigned long long *count, int64_t count_const, int cap,
                                                   Entry *refine, unsigned long long *refine_count, int fin_ins,
-                                                  long long *prof, unsigned long long *ticket) {
-    __shared__ long long next;
-    __shared__ uint64_t bar;  // run staging (TMA bulk copies) completion
+                                                  long long *prof, unsigned long long *ticket, int prefetch) {
+    __shared__ long long next, cur_s;
+    __shared__ uint64_t bar[2];  // run staging (TMA bulk copies) completion: keys, payload
     uint32_t parity = 0;
     const int64_t ne = count ? min((int64_t)*count, count_const) : count_const;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
     __syncthreads();
     if (!ticket) {  // one run per CTA (grid = exact count)
         if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
-                                                           fin_ins, prof, &bar, parity);
+                                                           fin_ins, prof, bar, parity);
         return;
     }
-    while (true) {  // dynamic scheduling: a CTA takes the next run as soon as it is free
-        if (threadIdx.x == 0) next = (long long)atomicAdd(ticket, 1ull);
+    // Dynamic scheduling with a lookahead of one run: a CTA holds the ticket
+    // of its next run while it finishes the current one and (`prefetch`: the
+    // level's records do not fit L2, so the scatter's evict_last runs are not
+    // all resident) has the copy engine prefetch that run's keys and payload
+    // into L2, so its staging copies hit L2 instead of waiting on HBM.
+    long long cur = 0;
+    if (threadIdx.x == 0) cur = (long long)atomicAdd(ticket, 1ull);
+    while (true) {
+        if (threadIdx.x == 0) {
+            const long long nx = (long long)atomicAdd(ticket, 1ull);
+            next = nx;
+            if (nx < ne && prefetch) finish_prefetch<PB>(B, entries[nx]);
+        }
+        if (threadIdx.x == 0) cur_s = cur;
         __syncthreads();
-        const int64_t i = next;
+        const int64_t i = cur_s;
+        cur = next;
         if (i >= ne) break;
-        finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof, &bar, parity);
+        finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof, bar, parity);
         __syncthreads();
     }
 }
