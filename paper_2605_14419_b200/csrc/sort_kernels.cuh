@@ -394,7 +394,10 @@ constexpr int CDF_KNOTS = 1024;  // coarse z-bins of the level-1 equalisation ta
 // 16-byte aligned and the launch provided the ring (stage_ok): the copy
 // engine keeps ~128 KB per SM in flight, which per-thread loads do not.
 constexpr int HIST_CHUNK = 4096;
-constexpr int HIST_STAGES = 4;
+#ifndef ZSB_HIST_STAGES
+#define ZSB_HIST_STAGES 4
+#endif
+constexpr int HIST_STAGES = ZSB_HIST_STAGES;
 
 __host__ __device__ inline size_t hist_smem(int kmax, bool ring) {
     size_t o = (size_t)((kmax + 1) & ~1) * 4 + (size_t)CDF_KNOTS * 8;
