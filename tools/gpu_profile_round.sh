@@ -15,3 +15,8 @@ $CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_level1_map|k_hist|k_scatter|k_classify|k_finish" -s 12 -c 6 \
     -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?"
+# the larger single-GPU workloads (C4 = 1e8 skewed float64, X9 = 1e9 uniform int64), bench lines only
+for C in 4 9; do
+  timeout -s KILL 900 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-comparators > gpurun_out/${TAG}_bench_c$C.json 2> gpurun_out/${TAG}_bench_c$C.err
+  echo "bench c$C rc=$?"
+done
