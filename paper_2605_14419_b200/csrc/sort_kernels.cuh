@@ -2022,7 +2022,18 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             const int c = z - a;
             int rank = i - a;
             if (c <= fin_ins) {
-                if (c > 1) {
+                if (c > 1 && c <= 4) {
+                    // the common sizes (S >= m/2 sub-buckets: ~1-3 records):
+                    // four masked compares, no loop; reads past z stay
+                    // inside the shared-memory allocation and are masked
+                    rank = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const uint64_t ox = Bo[a + q];
+                        if constexpr (PK) rank += (q < c) & (ox < pv);
+                        else rank += (q < c) & ((ox < ov) || (ox == ov && Ix[a + q] < idx));
+                    }
+                } else if (c > 4) {
                     rank = 0;
                     for (int x = a; x < z; x++) {
                         const uint64_t ox = Bo[x];
