@@ -1718,12 +1718,14 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     __syncthreads();
     FIN_MARK(7);  // staged
 
+    // items past the run end load a copy of the last key (no effect on the
+    // min/max); the histogram and the placement skip them.  A warp whose
+    // items all lie inside the run (`wfull`, all but the last warps) runs
+    // the unchecked loop bodies.
+    const bool wfull = (w + 1) * 32 * F <= m;
     uint64_t o[F];
 #pragma unroll
-    for (int j = 0; j < F; j++) {
-        const int i = base + j * 32;
-        o[j] = i < m ? kin[i] : 0ull;
-    }
+    for (int j = 0; j < F; j++) o[j] = kin[min(base + j * 32, m - 1)];
     if (tid == 0) nbig = 0;
     bool anyneg = false;
     if constexpr (KK == KEY_F64) {
@@ -1735,10 +1737,8 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
 #pragma unroll
     for (int j = 0; j < F; j++) {
         o[j] = ord_key<KK>(o[j]);
-        if (base + j * 32 < m) {
-            omin = min(omin, (unsigned long long)o[j]);
-            omax = max(omax, (unsigned long long)o[j]);
-        }
+        omin = min(omin, (unsigned long long)o[j]);
+        omax = max(omax, (unsigned long long)o[j]);
     }
     omin = warp_min_u64(omin);
     omax = warp_max_u64(omax);
@@ -1835,17 +1835,23 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     FIN_MARK(2);
     // ---- histogram (16-bit counters: no carry, counts <= cap < 2^16)
     uint32_t dpk[(F + 1) / 2];  // digits, two per register
-    auto hist_t = [&](auto vd_t) {
+    auto hist_t = [&](auto vd_t, auto full_t) {
+        constexpr bool FULL = decltype(full_t)::value;
 #pragma unroll
         for (int j = 0; j < F; j++) {
-            const int d = (base + j * 32 < m) ? digit_t(vd_t, o[j]) : 0xFFFF;
+            const int d = (FULL || base + j * 32 < m) ? digit_t(vd_t, o[j]) : 0xFFFF;
             if (j & 1) dpk[j >> 1] |= (uint32_t)d << 16;
             else dpk[j >> 1] = (uint32_t)d;
-            if (d != 0xFFFF) atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
+            if (FULL || d != 0xFFFF) atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
         }
     };
-    if (KK == KEY_F64 && vdig) hist_t(std::true_type{});
-    else hist_t(std::false_type{});
+    if (KK == KEY_F64 && vdig) {
+        if (wfull) hist_t(std::true_type{}, std::true_type{});
+        else hist_t(std::true_type{}, std::false_type{});
+    } else {
+        if (wfull) hist_t(std::false_type{}, std::true_type{});
+        else hist_t(std::false_type{}, std::false_type{});
+    }
     __syncthreads();
     FIN_MARK(3);
     // ---- exclusive scan of the counters in place (they become the cursors;
@@ -1908,11 +1914,11 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     const int nb = nbig;  // <= m / (fin_ins + 1) <= FIN_BIG_MAX
     FIN_MARK(4);
     // ---- place (atomic cursors; oversized digits go through the stable path)
-    auto place_t = [&](auto pk_t, auto big_t) {
+    auto place_t = [&](auto pk_t, auto big_t, auto full_t) {
 #pragma unroll
         for (int j = 0; j < F; j++) {
             const int d = (int)((dpk[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
-            bool go = d != 0xFFFF;
+            bool go = decltype(full_t)::value || d != 0xFFFF;
             if constexpr (decltype(big_t)::value) go = go && !((bigmask[d >> 5] >> (d & 31)) & 1u);
             if (go) {
                 const uint32_t old = atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
@@ -1928,11 +1934,12 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         }
     };
     if (packed) {
-        if (nb) place_t(std::true_type{}, std::true_type{});
-        else place_t(std::true_type{}, std::false_type{});
+        if (nb) place_t(std::true_type{}, std::true_type{}, std::false_type{});
+        else if (wfull) place_t(std::true_type{}, std::false_type{}, std::true_type{});
+        else place_t(std::true_type{}, std::false_type{}, std::false_type{});
     } else {
-        if (nb) place_t(std::false_type{}, std::true_type{});
-        else place_t(std::false_type{}, std::false_type{});
+        if (nb) place_t(std::false_type{}, std::true_type{}, std::false_type{});
+        else place_t(std::false_type{}, std::false_type{}, std::false_type{});
     }
     if (nb > 0) {
         // Stable placement of the oversized digits: sort their digit list,
