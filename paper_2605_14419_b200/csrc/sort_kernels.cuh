@@ -2018,8 +2018,14 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     // ---- rank inside each sub-bucket by (key, record index) and store to
     //      the final position; ties keep input order (stable)
     // (one loop per (packed, digit) combination: the flags are uniform per run)
-    auto rank_t = [&](auto pk_t, auto vd_t) {
+    auto rank_t = [&](auto pk_t, auto vd_t, auto neg_t) {
         constexpr bool PK = decltype(pk_t)::value;
+        // NEG = false: the run holds no -0.0 (checked once per run), so the
+        // key bits are the inverse ordered image with no per-record test
+        auto key_out = [&](uint64_t ov, int idx) -> uint64_t {
+            if constexpr (decltype(neg_t)::value) return key_bits(ov, idx);
+            else return key_from_ord<KK>(ov);
+        };
         for (int i = tid; i < m; i += FT) {
             const uint64_t pv = Bo[i];
             const uint64_t ov = PK ? (pv >> IB) + omin : pv;
@@ -2056,19 +2062,21 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
                     refine[r] = Entry{e.start + a, c, 2};
                 }
             }
-            ok[a + rank] = key_bits(ov, idx);
+            ok[a + rank] = key_out(ov, idx);
             if constexpr (PB != 0) op[a + rank] = pin[idx];
         }
     };
     mbar_wait(&bar[1], parity);  // payload staged (landed while the keys were ranked)
     parity ^= 1u;
     const bool vd = KK == KEY_F64 && vdig;
+    const bool neg = KK == KEY_F64 && anyneg;
     if (packed) {
-        if (vd) rank_t(std::true_type{}, std::true_type{});
-        else rank_t(std::true_type{}, std::false_type{});
+        if (vd) rank_t(std::true_type{}, std::true_type{}, std::true_type{});
+        else if (!neg) rank_t(std::true_type{}, std::false_type{}, std::false_type{});
+        else rank_t(std::true_type{}, std::false_type{}, std::true_type{});
     } else {
-        if (vd) rank_t(std::false_type{}, std::true_type{});
-        else rank_t(std::false_type{}, std::false_type{});
+        if (vd) rank_t(std::false_type{}, std::true_type{}, std::true_type{});
+        else rank_t(std::false_type{}, std::false_type{}, std::true_type{});
     }
     FIN_MARK(6);
 #undef FIN_MARK
