@@ -241,22 +241,25 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// 64-bit warp min/max from two 32-bit REDUX reductions (high words, then the
+// low words of the lanes holding the extreme high word); full warp only
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w < v ? w : v;
-    }
-    return v;
+    const unsigned hi = (unsigned)(v >> 32);
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? (unsigned)v : 0xffffffffu);
+    return ((unsigned long long)mh << 32) | ml;
 }
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w > v ? w : v;
-    }
-    return v;
+    const unsigned hi = (unsigned)(v >> 32);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)v : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
+// Sum of the 32-bit warp totals of the warps before warp w (one REDUX).
+__device__ __forceinline__ uint32_t warps_before(const uint32_t *wsum, int w, int lane) {
+    return __reduce_add_sync(0xffffffffu, lane < w ? wsum[lane] : 0u);
 }
 
 // Named barriers 1..15 (0 is __syncthreads).

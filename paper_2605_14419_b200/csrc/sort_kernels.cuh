@@ -676,8 +676,7 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
     }
     if (lane == 31) wsum[w] = x;
     __syncthreads();
-    uint32_t run = x - tsum;
-    for (int q = 0; q < w; q++) run += wsum[q];
+    uint32_t run = x - tsum + warps_before(wsum, w, lane);
     for (int d = d0; d < d1; d++) {
         dstart[d] = (uint16_t)run;
 #pragma unroll
@@ -1881,8 +1880,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
         }
         if (lane == 31) wsum[w] = x;
         __syncthreads();
-        uint32_t run = x - tsum;
-        for (int q = 0; q < w; q++) run += wsum[q];
+        uint32_t run = x - tsum + warps_before(wsum, w, lane);
         auto excl = [&](uint32_t v, int d) -> uint32_t {  // start of digit d (count v); flags oversized
             const uint32_t st = run;
             if (v > (uint32_t)fin_ins) {
