@@ -82,7 +82,11 @@ size_t zsb_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, 
  * payload (payload_bytes 0/4/8; d_payload/d_out_payload may be NULL when 0).
  * Replaces core.zsort -> _kernels.zsort_driver (core.py:348-400,
  * _kernels.py:393-450).  h_stats (may be NULL) receives ZSB_STAT_SLOTS
- * int64 counters; the call blocks until the sort has completed. */
+ * int64 counters; with h_stats the call blocks until the sort has completed.
+ * With h_stats == NULL the call is stream-ordered: it returns once the last
+ * partition level is enqueued on `stream` (a sort with several levels still
+ * waits on the host for each level's outcome), so callers synchronise on
+ * the stream like after any CUDA library call. */
 int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
              void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
              int64_t *h_stats, void *stream);

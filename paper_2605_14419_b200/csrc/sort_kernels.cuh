@@ -2093,32 +2093,18 @@ __device__ __forceinline__ void finish_prefetch(const Buffers &B, const Entry e)
     }
 }
 
-// Persistent finish: the work count is read from device memory (written by
-// the classify or a previous finish), so the host enqueues without a sync.
+// Persistent finish over one run list; dynamic scheduling with a lookahead
+// of one run: a CTA holds the ticket of its next run while it finishes the
+// current one and (`prefetch`: the level's records do not fit L2, so the
+// scatter's evict_last runs are not all resident) has the copy engine
+// prefetch that run's keys and payload into L2, so its staging copies hit L2
+// instead of waiting on HBM.
 template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
-                                                  const unsigned long long *count, int64_t count_const, int cap,
-                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
-                                                  long long *prof, unsigned long long *ticket, int prefetch) {
+__device__ __forceinline__ void finish_list(const Buffers &B, const Entry *__restrict__ entries, int64_t ne, int cap,
+                                            Entry *refine, unsigned long long *refine_count, int fin_ins,
+                                            long long *prof, unsigned long long *ticket, int prefetch, uint64_t *bar,
+                                            uint32_t &parity) {
     __shared__ long long next, cur_s;
-    __shared__ uint64_t bar[2];  // run staging (TMA bulk copies) completion: keys, payload
-    uint32_t parity = 0;
-    const int64_t ne = count ? min((int64_t)*count, count_const) : count_const;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-    }
-    __syncthreads();
-    if (!ticket) {  // one run per CTA (grid = exact count)
-        if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
-                                                           fin_ins, prof, bar, parity);
-        return;
-    }
-    // Dynamic scheduling with a lookahead of one run: a CTA holds the ticket
-    // of its next run while it finishes the current one and (`prefetch`: the
-    // level's records do not fit L2, so the scatter's evict_last runs are not
-    // all resident) has the copy engine prefetch that run's keys and payload
-    // into L2, so its staging copies hit L2 instead of waiting on HBM.
     long long cur = 0;
     if (threadIdx.x == 0) cur = (long long)atomicAdd(ticket, 1ull);
     while (true) {
@@ -2134,6 +2120,70 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
         if (i >= ne) break;
         finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof, bar, parity);
         __syncthreads();
+    }
+}
+
+// Persistent finish: the work count is read from device memory (written by
+// the classify or a previous finish), so the host enqueues without a sync.
+template <int KK, int PB>
+__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
+                                                  const unsigned long long *count, int64_t count_const, int cap,
+                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
+                                                  long long *prof, unsigned long long *ticket, int prefetch) {
+    __shared__ uint64_t bar[2];  // run staging (TMA bulk copies) completion: keys, payload
+    uint32_t parity = 0;
+    const int64_t ne = count ? min((int64_t)*count, count_const) : count_const;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    if (!ticket) {  // one run per CTA (grid = exact count)
+        if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
+                                                           fin_ins, prof, bar, parity);
+        return;
+    }
+    finish_list<KK, PB>(B, entries, ne, cap, refine, refine_count, fin_ins, prof, ticket, prefetch, bar, parity);
+}
+
+// Refine pass (cooperative launch, every CTA resident): finishes the refine
+// runs of a finish (list A, count *count_a) into list B, then B into A, ...
+// until a pass leaves none, so oversized sub-buckets of refine runs never
+// need the host.  Each pass's run count is added to *runs_total (SortStats).
+// Lists and counts are swapped between passes; a pass's input count and the
+// ticket are reset by block 0 between the two grid barriers.
+template <int KK, int PB>
+__global__ void __launch_bounds__(FT, 1) k_refine(Buffers B, Entry *list_a, unsigned long long *count_a, Entry *list_b,
+                                                  unsigned long long *count_b, int64_t cap_list, int cap, int fin_ins,
+                                                  unsigned long long *ticket, unsigned long long *runs_total,
+                                                  int prefetch) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint64_t bar[2];
+    uint32_t parity = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    Entry *lin = list_a, *lout = list_b;
+    unsigned long long *cin = count_a, *cout = count_b;
+    while (true) {
+        const int64_t ne = min((int64_t)*(volatile unsigned long long *)cin, cap_list);
+        if (ne == 0) break;  // every CTA reads the same value (written before the last grid barrier)
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(runs_total, (unsigned long long)ne);
+        finish_list<KK, PB>(B, lin, ne, cap, lout, cout, fin_ins, nullptr, ticket, prefetch, bar, parity);
+        grid.sync();  // pass done: its refine runs are all in lout
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            *cin = 0ull;
+            *ticket = 0ull;
+        }
+        grid.sync();
+        Entry *tl = lin;
+        lin = lout;
+        lout = tl;
+        unsigned long long *tc = cin;
+        cin = cout;
+        cout = tc;
     }
 }
 

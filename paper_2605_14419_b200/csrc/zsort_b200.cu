@@ -462,12 +462,38 @@ int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev
         PhaseScope ph(PH_FINISH, c.st);
         k_finish<KK, PB><<<(unsigned)grid, FT, FL.total, c.st>>>(c.B, list, count_dev, count_const, (int)c.P.cap, refine,
                                                                 ctrl + REF_SLOT[ref_out],
-                                                                env_int("ZSB_FIN_INS", FIN_INS),
+                                                                FIN_INS,  // refine lists hold <= n / (FIN_INS + 1) runs
                                                                 fin_prof(count_bound),
                                                                 count_dev ? ctrl + TICK_SLOT[tick] : nullptr,
                                                                 fin_prefetch(c.n, PB));
     }
     ZSB_LAUNCH("k_finish");
+    return ZSB_OK;
+}
+
+// Refine pass of a level (parity `par`): the refine runs its finish left in
+// list 2*par, and their own refine runs, ping-ponging between lists 2*par and
+// 2*par + 1 on the device until a pass leaves none (cooperative launch, one
+// CTA per SM; the finish's shared memory admits no second CTA).
+template <int KK, int PB>
+int launch_refine(Ctx &c, int par) {
+    FinLayout FL = fin_layout((int)c.P.cap, PB);
+    smem_optin(k_refine<KK, PB>, FL.total);
+    unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+    Entry *la = (Entry *)(c.ws + c.L.refine[2 * par]), *lb = (Entry *)(c.ws + c.L.refine[2 * par + 1]);
+    unsigned long long *ca = ctrl + REF_SLOT[2 * par], *cb = ctrl + REF_SLOT[2 * par + 1];
+    unsigned long long *tick = ctrl + TICK_SLOT[2 * par + 1], *tot = ctrl + C_ST_INSERTION;
+    int64_t cl = c.L.ref_cap;
+    int cap = (int)c.P.cap, fi = FIN_INS;
+    int pf = fin_prefetch(c.n, PB);
+    Buffers Bv = c.B;
+    void *args[] = {&Bv, &la, &ca, &lb, &cb, &cl, &cap, &fi, &tick, &tot, &pf};
+    {
+        PhaseScope ph(PH_FINISH, c.st);
+        ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_refine<KK, PB>, dim3(num_sms()), dim3(FT), args, FL.total,
+                                             c.st));
+    }
+    ZSB_LAUNCH("k_refine");
     return ZSB_OK;
 }
 
@@ -521,40 +547,29 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         return ZSB_OK;
     };
 
-    // Finish the runs of `list` and, right behind, their refine runs (one
-    // pass, count on the device) without a host round trip; parity `par`
-    // selects the refine lists.
+    // Finish the runs of `list` and, right behind, their refine runs (device
+    // iteration, count on the device) without a host round trip; parity
+    // `par` selects the refine lists.
     auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
                               int64_t bound, int par, bool zeroed = false) -> int {
         if (!zeroed) ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[2 * par], 0, 32, c.st));  // two counts, two tickets
         int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par);
         if (rc) return rc;
-        return launch_finish<KK, PB>(c, (const Entry *)(c.ws + c.L.refine[2 * par]), ctrl + REF_SLOT[2 * par],
-                                     c.L.ref_cap, std::min<int64_t>(bound, c.L.ref_cap), 2 * par + 1, 2 * par + 1);
+        return launch_refine<KK, PB>(c, par);
     };
-    // Refine runs of refine runs (rare): finished from list 2*par + 1 with
-    // host round trips, ping-ponging inside the parity's pair of lists.
-    auto drain_refine = [&](int par, int64_t pending) -> int {
-        int src = 2 * par + 1;
-        while (pending > 0) {
-            if (pending > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-            const int dst = src ^ 1;
-            ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[dst], 0, 8, c.st));
-            int rc = launch_finish<KK, PB>(c, (const Entry *)(c.ws + c.L.refine[src]), nullptr, pending, pending, dst, 0);
-            if (rc) return rc;
-            stats[ZSB_STAT_INSERTION] += pending;
-            if ((rc = full_sync())) return rc;
-            src = dst;
-            pending = (int64_t)hc[REF_SLOT[src]];
+    // The sort is stream-ordered: once its last level is enqueued the call
+    // returns, unless the caller asked for SortStats (or phase timing is on),
+    // which needs one host round trip (~18 us on B200).
+    auto finish_call = [&]() -> int {
+        if (h_stats || g_t.on) {
+            if (int rc = full_sync()) return rc;
+            stats[ZSB_STAT_INSERTION] += (int64_t)hc[C_ST_INSERTION];  // refine runs
+            stats[ZSB_STAT_MAX_DEPTH] = (int64_t)hc[C_ST_MAXDEPTH];
+            stats[ZSB_STAT_FALLBACKS] = (int64_t)hc[C_ST_FALLBACKS];
+            stats[ZSB_STAT_SCATTERS] = (int64_t)hc[C_ST_SCATTERS];
         }
+        if (h_stats) memcpy(h_stats, stats, sizeof(stats));
         return ZSB_OK;
-    };
-    // Counts of a level's finish passes (read after they completed).
-    auto settle_level = [&](int par) -> int {
-        const int64_t n0 = (int64_t)hc[REF_SLOT[2 * par]], n1 = (int64_t)hc[REF_SLOT[2 * par + 1]];
-        if (n0 > c.L.ref_cap || n1 > c.L.ref_cap) return fail(ZSB_ERR_WORKSPACE, "refine list overflow");
-        stats[ZSB_STAT_INSERTION] += n0;
-        return drain_refine(par, n1);
     };
 
     if (n <= c.P.cap) {  // one shared-memory finish (core.py:369-374; threshold widened to the smem capacity)
@@ -564,11 +579,9 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         }
         ZSB_LAUNCH("k_single_entry");
         int rc = enqueue_finish(entries, nullptr, 1, 1, 0);
-        if (rc || (rc = full_sync())) return rc;
+        if (rc) return rc;
         stats[ZSB_STAT_INSERTION] = 1;
-        if ((rc = settle_level(0))) return rc;
-        if (h_stats) memcpy(h_stats, stats, sizeof(stats));
-        return ZSB_OK;
+        return finish_call();
     }
 
     MapCfg mc{cfg.mapping, (int32_t)cfg.depth_guard};
@@ -673,11 +686,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         if (env_int("ZSB_DEBUG", 0))
             fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %lld entries %lld fallbacks %llu\n",
                     level, nseg, (long long)tiles, kmax, (long long)nchild, (long long)nentry, hc[C_ST_FALLBACKS]);
-        if (level > 1 && (rc = settle_level(par ^ 1))) return rc;  // the previous level's passes are done
-        if (nchild == 0) {
-            if ((rc = full_sync()) || (rc = settle_level(par))) return rc;
-            break;
-        }
+        if (nchild == 0) break;
         if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
         nseg = (int)nchild;
         tiles = (int64_t)hc[C_TILES_NEXT];
@@ -696,11 +705,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         fin_prof_dump();
         scat_prof_dump();
     }
-    stats[ZSB_STAT_MAX_DEPTH] = (int64_t)hc[C_ST_MAXDEPTH];
-    stats[ZSB_STAT_FALLBACKS] = (int64_t)hc[C_ST_FALLBACKS];
-    stats[ZSB_STAT_SCATTERS] = (int64_t)hc[C_ST_SCATTERS];
-    if (h_stats) memcpy(h_stats, stats, sizeof(stats));
-    return ZSB_OK;
+    return finish_call();
 }
 
 int check_common(const void *d_keys, int32_t kd, int32_t pb, int64_t n) {
