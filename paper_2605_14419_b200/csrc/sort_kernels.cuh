@@ -614,7 +614,10 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 // semantics of scatter_pass (_kernels.py:124-133), with no cross-warp
 // serialization.
 
-constexpr int SCAT_ITEMS = 16;
+#ifndef ZSB_SCAT_ITEMS
+#define ZSB_SCAT_ITEMS 16
+#endif
+constexpr int SCAT_ITEMS = ZSB_SCAT_ITEMS;
 constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
 // SW warps per CTA: 8 (4096-record rounds, two CTAs per SM) for k <= 1024,
 // 16 (8192-record rounds, one CTA per SM) above, so that a bucket's run in a

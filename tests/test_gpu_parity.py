@@ -37,11 +37,12 @@ def assert_matches_oracle(Z, keys, payload=None, config=None):
     keys = np.ascontiguousarray(keys)
     if payload is None:
         payload = np.arange(keys.size, dtype=np.int64)
-    ok, op, _ = Z.zsort(keys, payload, config)
+    ok, op, st = Z.zsort(keys, payload, config)
     ek, ep, _ = O.stable_sort(keys, payload)
     assert ok.dtype == keys.dtype
     np.testing.assert_array_equal(ok.view(np.uint64), ek.view(np.uint64))
     np.testing.assert_array_equal(op, ep)
+    return ok, op, st
 
 
 # ------------------------------------------------ reference unit tests
@@ -377,3 +378,57 @@ def test_scatter_tie_paths(Z, tie_check, monkeypatch):
     assert_matches_oracle(Z, few)
     runs = np.repeat(rng.standard_normal(20_000), 100)  # sorted-run-like ties inside warps
     assert_matches_oracle(Z, runs)
+
+
+def _nested_scales(rng, n, levels, outliers=12):
+    """Keys whose range is stretched by a few outliers at every scale: the
+    bulk of each finish run lands in one sub-bucket (an oversized digit), and
+    the refine run of that digit is stretched again by the next scale's
+    outliers, so refine runs produce refine runs (the device ping-pong)."""
+    keys = rng.integers(0, 1000, size=n, dtype=np.int64)
+    pos = rng.permutation(n)
+    at = 0
+    for lv in range(levels):
+        scale = 10 ** (3 * (lv + 1))
+        sel = pos[at:at + outliers]
+        keys[sel] = rng.integers(scale, min(10 * scale, 2**62), size=sel.size, dtype=np.int64)
+        at += outliers
+    return keys
+
+
+@pytest.mark.parametrize("n,levels", [(12000, 5), (8000, 6), (200_000, 5), (3_000_000, 4)])
+def test_nested_refine_runs(Z, n, levels):
+    rng = np.random.default_rng(1000 + levels)
+    keys = _nested_scales(rng, n, levels)
+    ok, op, st = assert_matches_oracle(Z, keys)
+    if n <= 12000:  # one shared-memory finish: every further run is a refine run
+        assert st.insertion_sort_invocations > 2, st
+
+
+def test_stream_ordered_without_stats(Z):
+    """zsb_sort with no stats buffer returns once the sort is enqueued; after a
+    stream sync the output equals the synchronous call's."""
+    import ctypes
+    from paper_2605_14419_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(77)
+    keys = torch.from_numpy(rng.standard_normal(3_000_000)).cuda()
+    pay = torch.arange(keys.numel(), dtype=torch.int32, device="cuda")
+    c = Z.SortConfig().to_c()
+    n = keys.numel()
+    ws_bytes = L.zsb_workspace_bytes(n, 1, 4, c)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    outs = []
+    for with_stats in (True, False):
+        ok, op = torch.empty_like(keys), torch.empty_like(pay)
+        stats = (ctypes.c_int64 * 5)() if with_stats else None
+        rc = L.zsb_sort(keys.data_ptr(), 1, pay.data_ptr(), 4, ok.data_ptr(), op.data_ptr(), n, c, ws.data_ptr(),
+                        ws_bytes, stats, torch.cuda.current_stream().cuda_stream)
+        _lib.check(rc)
+        torch.cuda.current_stream().synchronize()
+        outs.append((ok.cpu().numpy(), op.cpu().numpy()))
+    assert np.array_equal(outs[0][0].view(np.uint64), outs[1][0].view(np.uint64))
+    assert np.array_equal(outs[0][1], outs[1][1])
+    ek, ep, _ = O.stable_sort(keys.cpu().numpy(), pay.cpu().numpy())
+    assert np.array_equal(outs[1][1], ep)
