@@ -64,7 +64,7 @@ struct SegParams {
     int32_t shift;     // integer mode: digit = (ord - umin) >> shift
     int32_t src;       // buffer holding the segment: 0 = input, 1 = tmp, 2 = out
     int32_t kf;        // MODE_ZCDF: coarse z-bins of the CDF table (scale is the coarse scale)
-    int32_t pad;
+    int32_t win;       // finish window width of the segment's buckets (0: the level default)
     float za, zb;      // MODE_ZCDF: coarse coordinate = fmaf((float)(x - center), za, zb)
 };
 

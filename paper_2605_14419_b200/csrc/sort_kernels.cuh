@@ -1291,6 +1291,8 @@ struct ClassCfg {
     int32_t half;  // window
     int32_t depth_guard;
     int32_t mapping;
+    int32_t child_fill;  // recursion children: k = pow2 >= child_fill * len / cap (buckets ~ cap / child_fill)
+    int32_t greedy;      // recursion levels pack finish runs greedily (else fixed windows)
 };
 
 __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64_t g) {
@@ -1387,7 +1389,8 @@ __device__ __forceinline__ int window_item(int64_t g, const SegParams *__restric
     if (p.mode == MODE_COPY) return 0;
     const int64_t w = g - wfirst[s];
     const int64_t *bs = bs_one ? bs_one : bstart + kfirst[s];  // k + 1 slots (a shared copy for one segment)
-    const int64_t ws = p.start + w * cc.half, we = ws + cc.half;
+    const int64_t W = p.win > 0 ? p.win : cc.half;
+    const int64_t ws = p.start + w * W, we = ws + W;
     const int b0 = lower_bound_i64(bs, p.k, ws);
     const int b1 = lower_bound_i64(bs, p.k, we);
     if (b0 >= b1) return 0;  // no bucket starts inside this window
@@ -1395,7 +1398,7 @@ __device__ __forceinline__ int window_item(int64_t g, const SegParams *__restric
     const int64_t last = bs[b1] - bs[b1 - 1];
     int64_t e0 = bs[b0], e1 = bs[b1];
     int ne = 0;
-    if (last > cc.cap - cc.half) {
+    if (last > cc.cap - W) {
         e1 = bs[b1 - 1];
         if (last <= cc.cap) e[ne++] = Entry{bs[b1 - 1], (int32_t)last, dst};  // a mid-size bucket is a run of its own
     }
@@ -1408,8 +1411,40 @@ __device__ __forceinline__ int window_item(int64_t g, const SegParams *__restric
 // (single CTA; the child count is read from the control block).  k is sized
 // to the child so its buckets average ~cap/4 records (the reference's fixed
 // k across levels is a CPU choice, core.py:355).
+// Greedy finish runs of one segment (one warp): consecutive buckets join the
+// current run while it stays within `cap` records; a bucket above `cap` is a
+// child (recursed) and closes the run.  Runs fill to ~cap - a/2 for a mean
+// bucket of a records (fixed windows reach only cap - a).  Each ballot finds
+// the next bucket that breaks the run, so a chunk of 32 buckets costs one
+// step per run it closes.
+__device__ __forceinline__ void greedy_runs(const SegParams &p, const int64_t *__restrict__ bs, int cap,
+                                            Entry *entries, unsigned long long *nentry, int lane) {
+    const int dst = (p.src == 1) ? 2 : 1;
+    const int k = p.k;
+    int64_t R = bs[0];  // start of the open run (a bucket boundary)
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        const int i = c0 + lane;
+        const int64_t st = i < k ? bs[i] : 0, en = i < k ? bs[i + 1] : 0;
+        int from = 0;
+        while (true) {
+            const bool valid = lane >= from && i < k;
+            const bool brk = valid && (en - st > cap || en - R > cap);
+            const unsigned m = __ballot_sync(0xffffffffu, brk);
+            if (!m) break;  // the rest of the chunk joins the open run
+            const int f = __ffs(m) - 1;
+            const int64_t sf = __shfl_sync(0xffffffffu, st, f), ef = __shfl_sync(0xffffffffu, en, f);
+            const bool child = ef - sf > cap;
+            if (lane == 0 && sf > R) entries[atomicAdd(nentry, 1ull)] = Entry{R, (int32_t)(sf - R), dst};
+            R = child ? ef : sf;  // a child is skipped; else bucket f opens the next run
+            from = child ? f + 1 : f;
+        }
+    }
+    if (lane == 0 && bs[k] > R) entries[atomicAdd(nentry, 1ull)] = Entry{R, (int32_t)(bs[k] - R), dst};
+}
+
 __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, int64_t *kfirst, int64_t *wfirst,
-                           unsigned long long *ctrl, int32_t cap, int32_t half, int32_t kmax_child, int32_t min_tile) {
+                           unsigned long long *ctrl, int32_t cap, int32_t half, int32_t kmax_child, int32_t min_tile,
+                           int32_t child_fill) {
     const int nseg = (int)*(volatile const unsigned long long *)nseg_ptr;
     constexpr int NV = 4;  // tiles, matrix entries, records, bucket slots, windows -> 5 with windows
     __shared__ long long sh[5][32];
@@ -1442,7 +1477,7 @@ __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, 
         SegParams p;
         if (s < nseg) {
             p = segs[s];
-            int64_t want = (p.len * 4 + cap - 1) / cap;
+            int64_t want = (p.len * child_fill + cap - 1) / cap;
             int k = 16;
             while (k < want && k < kmax_child) k <<= 1;
             p.k = k;
@@ -1450,11 +1485,21 @@ __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, 
             tl = (tl + 255) & ~(int64_t)255;
             p.tile_len = tl;
             p.ntiles = (int32_t)((p.len + tl - 1) / tl);
+            // finish windows sized to the children's mean bucket a: a run is
+            // the buckets starting in a window of cap - 1.3a records plus the
+            // last of them when it has <= 1.3a records, so runs fill to
+            // ~cap - 0.3a whatever the bucket size
+            {
+                const int64_t a = p.len / k;
+                int64_t W = (int64_t)cap - (a * 13) / 10;
+                W = min((int64_t)cap - 256, max((int64_t)cap / 4, W));
+                p.win = (int32_t)W;
+            }
             v[0] = p.ntiles;
             v[1] = (long long)p.ntiles * k;
             v[2] = p.len;
             v[3] = k + 1;
-            v[4] = (p.len + half - 1) / half;
+            v[4] = (p.len + p.win - 1) / p.win;
             atomicMax(&kmax, k);
         }
         long long x[5];
@@ -1525,9 +1570,18 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
         __syncthreads();
         bs_one = bs_sh;
     }
+    const int lane = lane_id();
+    if (nseg > 1 && cc.greedy) {
+        // recursion levels: greedy runs per segment, one warp each
+        for (int64_t sg = g0 >> 5; sg < nseg; sg += G >> 5) {
+            const SegParams p = segs[sg];
+            if (p.mode == MODE_COPY) continue;
+            greedy_runs(p, bstart + kfirst[sg], cc.cap, entries, &ctrl[C_NENTRY], lane);
+        }
+        total_windows = 0;
+    }
     // windows: whole warps iterate together so each warp appends its entries
     // with one atomic (the entry counter is otherwise a hot spot)
-    const int lane = lane_id();
     for (int64_t gw = g0 - lane; gw < total_windows; gw += G) {
         Entry e[2];
         const int ne = gw + lane < total_windows
@@ -1547,7 +1601,8 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
     }
     grid.sync();
     if (blockIdx.x == 0)
-        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, cc.half, kmax_child, min_tile);
+        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, cc.half, kmax_child, min_tile,
+                   cc.child_fill);
 }
 
 // ------------------------------------------------------------------- K5

@@ -585,7 +585,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     }
 
     MapCfg mc{cfg.mapping, (int32_t)cfg.depth_guard};
-    ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping};
+    ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping,
+                (int32_t)std::max(1, std::min(16, env_int("ZSB_CHILD_FILL", 2))), env_int("ZSB_GREEDY", 1)};
     const int64_t nwin1 = (n + c.P.half - 1) / c.P.half;
     const bool equalize = cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0);
     unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
