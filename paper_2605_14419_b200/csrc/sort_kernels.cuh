@@ -1282,13 +1282,14 @@ __global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ 
 //   bstart[kfirst[s] + b] (k_s + 1 slots per segment, last = segment end);
 //   buckets above capacity become next-level segments centred on the
 //   bucket's estimated mean (_kernels.py:103-106, 282-318).
-// k_windows: one thread per (segment, window of `half` records): the buckets
-//   whose start lies in the window form one finish run (<= cap records),
-//   found by binary search over bstart -- no serial walks over empty tails.
+// runs, level 1 (one segment): one thread per window of `half` records: the
+//   buckets whose start lies in the window form one finish run (<= cap
+//   records), found by binary search over bstart;
+// runs, recursion levels: greedy_runs, one warp per segment.
 
 struct ClassCfg {
     int32_t cap;   // finish capacity (records)
-    int32_t half;  // window
+    int32_t half;  // level-1 window (recursion segments carry their own in SegParams::win)
     int32_t depth_guard;
     int32_t mapping;
     int32_t child_fill;  // recursion children: k = pow2 >= child_fill * len / cap (buckets ~ cap / child_fill)
@@ -1443,7 +1444,7 @@ __device__ __forceinline__ void greedy_runs(const SegParams &p, const int64_t *_
 }
 
 __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, int64_t *kfirst, int64_t *wfirst,
-                           unsigned long long *ctrl, int32_t cap, int32_t half, int32_t kmax_child, int32_t min_tile,
+                           unsigned long long *ctrl, int32_t cap, int32_t kmax_child, int32_t min_tile,
                            int32_t child_fill) {
     const int nseg = (int)*(volatile const unsigned long long *)nseg_ptr;
     constexpr int NV = 4;  // tiles, matrix entries, records, bucket slots, windows -> 5 with windows
@@ -1601,8 +1602,7 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
     }
     grid.sync();
     if (blockIdx.x == 0)
-        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, cc.half, kmax_child, min_tile,
-                   cc.child_fill);
+        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, kmax_child, min_tile, cc.child_fill);
 }
 
 // ------------------------------------------------------------------- K5
