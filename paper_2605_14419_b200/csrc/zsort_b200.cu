@@ -353,6 +353,17 @@ int scatter_tie_check() {
     return dev_flag[dev];
 }
 
+// L2 prefetch of the next finish run by the copy engine: only when the
+// level's records exceed the L2; below it the scatter's evict_last runs are
+// still resident and the prefetch only adds traffic (measured on B200: C2
+// +5 us, C4 -47 us).  (The same prefetch of the scatter's next round of keys
+// won 1 % at C4/X9 but cost C2 its register allocation: not used.)
+int fin_prefetch(int64_t n, int pb) {
+    const int forced = env_int("ZSB_L2_PREFETCH", -1);
+    if (forced >= 0) return forced;
+    return (double)n * (8 + pb) > 128.0 * (1 << 20) ? 1 : 0;
+}
+
 template <int KK, int PB>
 int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
                      bool segs_level1 = false, cudaEvent_t after_scan = nullptr) {
@@ -429,15 +440,6 @@ void fin_prof_dump() {
     cudaFree(g_fin_prof);
     g_fin_prof = nullptr;
     g_fin_prof_n = 0;
-}
-
-// L2 prefetch of the next finish run: only when the records exceed the L2
-// (below it the scatter's evict_last runs are still resident and the
-// prefetch only adds traffic; measured on B200: C2 +5 us, C4 -47 us).
-int fin_prefetch(int64_t n, int pb) {
-    const int forced = env_int("ZSB_FIN_PREFETCH", -1);
-    if (forced >= 0) return forced;
-    return (double)n * (8 + pb) > 128.0 * (1 << 20) ? 1 : 0;
 }
 
 // Refine lists: two per level parity (a level's finish writes list 2*par,
