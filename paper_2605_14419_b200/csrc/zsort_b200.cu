@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -686,9 +687,15 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         }
         stats[ZSB_STAT_INSERTION] += nentry;
         const int64_t nchild = (int64_t)hc[C_NCHILD];
-        if (env_int("ZSB_DEBUG", 0))
-            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %lld entries %lld fallbacks %llu\n",
-                    level, nseg, (long long)tiles, kmax, (long long)nchild, (long long)nentry, hc[C_ST_FALLBACKS]);
+        if (env_int("ZSB_DEBUG", 0)) {  // host time since the call started: when this level's classify was seen
+            static thread_local std::chrono::steady_clock::time_point t_call;
+            if (level == 1) t_call = std::chrono::steady_clock::now();
+            const double us =
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count();
+            fprintf(stderr, "[zsb] level %d: nseg %d tiles %lld kmax %d -> children %lld entries %lld fallbacks %llu"
+                            " (host +%.0f us)\n",
+                    level, nseg, (long long)tiles, kmax, (long long)nchild, (long long)nentry, hc[C_ST_FALLBACKS], us);
+        }
         if (nchild == 0) break;
         if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
         nseg = (int)nchild;
