@@ -23,7 +23,10 @@ namespace zsb {
 
 constexpr int NT = 256;        // threads per CTA for the streaming kernels
 constexpr int NWARPS = NT / 32;
-constexpr int SCAN_ITEMS = 16;  // entries per thread in k_scan
+#ifndef ZSB_SCAN_ITEMS
+#define ZSB_SCAN_ITEMS 16
+#endif
+constexpr int SCAN_ITEMS = ZSB_SCAN_ITEMS;  // entries per thread in k_scan
 constexpr int SCAN_TILE = NT * SCAN_ITEMS;
 
 struct Buffers {
