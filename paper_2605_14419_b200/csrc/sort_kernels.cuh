@@ -2184,48 +2184,18 @@ __device__ __forceinline__ void finish_list(const Buffers &B, const Entry *__res
     }
 }
 
-// Persistent finish: the work count is read from device memory (written by
-// the classify or a previous finish), so the host enqueues without a sync.
-template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
-                                                  const unsigned long long *count, int64_t count_const, int cap,
-                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
-                                                  long long *prof, unsigned long long *ticket, int prefetch) {
-    __shared__ uint64_t bar[2];  // run staging (TMA bulk copies) completion: keys, payload
-    uint32_t parity = 0;
-    const int64_t ne = count ? min((int64_t)*count, count_const) : count_const;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-    }
-    __syncthreads();
-    if (!ticket) {  // one run per CTA (grid = exact count)
-        if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
-                                                           fin_ins, prof, bar, parity);
-        return;
-    }
-    finish_list<KK, PB>(B, entries, ne, cap, refine, refine_count, fin_ins, prof, ticket, prefetch, bar, parity);
-}
-
-// Refine pass (cooperative launch, every CTA resident): finishes the refine
-// runs of a finish (list A, count *count_a) into list B, then B into A, ...
-// until a pass leaves none, so oversized sub-buckets of refine runs never
-// need the host.  Each pass's run count is added to *runs_total (SortStats).
-// Lists and counts are swapped between passes; a pass's input count and the
+// Refine iterations (every CTA of a cooperative grid): finishes the refine
+// runs in list A (count *count_a) into list B, then B into A, ... until a
+// pass leaves none, so oversized sub-buckets of refine runs never need the
+// host.  Each pass's run count is added to *runs_total (SortStats).  Lists
+// and counts are swapped between passes; a pass's input count and the
 // ticket are reset by block 0 between the two grid barriers.
 template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 1) k_refine(Buffers B, Entry *list_a, unsigned long long *count_a, Entry *list_b,
-                                                  unsigned long long *count_b, int64_t cap_list, int cap, int fin_ins,
-                                                  unsigned long long *ticket, unsigned long long *runs_total,
-                                                  int prefetch) {
+__device__ void refine_loop(const Buffers &B, Entry *list_a, unsigned long long *count_a, Entry *list_b,
+                            unsigned long long *count_b, int64_t cap_list, int cap, int fin_ins,
+                            unsigned long long *ticket, unsigned long long *runs_total, int prefetch, uint64_t *bar,
+                            uint32_t &parity) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint64_t bar[2];
-    uint32_t parity = 0;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-    }
-    __syncthreads();
     Entry *lin = list_a, *lout = list_b;
     unsigned long long *cin = count_a, *cout = count_b;
     while (true) {
@@ -2246,6 +2216,63 @@ __global__ void __launch_bounds__(FT, 1) k_refine(Buffers B, Entry *list_a, unsi
         cin = cout;
         cout = tc;
     }
+}
+
+struct RefineArgs {  // the refine iterations a finish launch runs after its own list (list_b == nullptr: none)
+    Entry *list_b;
+    unsigned long long *count_b;
+    int64_t cap_list;
+    unsigned long long *ticket_b;
+    unsigned long long *runs_total;
+};
+
+// Persistent finish: the work count is read from device memory (written by
+// the classify or a previous finish), so the host enqueues without a sync.
+// With `ra.list_b` (cooperative launch) the same grid then runs the refine
+// iterations of the runs it left in `refine`: one launch per level instead
+// of two.
+template <int KK, int PB>
+__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
+                                                  const unsigned long long *count, int64_t count_const, int cap,
+                                                  Entry *refine, unsigned long long *refine_count, int fin_ins,
+                                                  long long *prof, unsigned long long *ticket, int prefetch,
+                                                  RefineArgs ra) {
+    __shared__ uint64_t bar[2];  // run staging (TMA bulk copies) completion: keys, payload
+    uint32_t parity = 0;
+    const int64_t ne = count ? min((int64_t)*count, count_const) : count_const;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    if (!ticket) {  // one run per CTA (grid = exact count)
+        if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
+                                                           fin_ins, prof, bar, parity);
+    } else {
+        finish_list<KK, PB>(B, entries, ne, cap, refine, refine_count, fin_ins, prof, ticket, prefetch, bar, parity);
+    }
+    if (ra.list_b) {
+        cg::this_grid().sync();  // every refine run of the list is published
+        refine_loop<KK, PB>(B, refine, refine_count, ra.list_b, ra.count_b, ra.cap_list, cap, fin_ins, ra.ticket_b,
+                            ra.runs_total, prefetch, bar, parity);
+    }
+}
+
+// Refine pass as a launch of its own (cooperative, every CTA resident).
+template <int KK, int PB>
+__global__ void __launch_bounds__(FT, 1) k_refine(Buffers B, Entry *list_a, unsigned long long *count_a, Entry *list_b,
+                                                  unsigned long long *count_b, int64_t cap_list, int cap, int fin_ins,
+                                                  unsigned long long *ticket, unsigned long long *runs_total,
+                                                  int prefetch) {
+    __shared__ uint64_t bar[2];
+    uint32_t parity = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    refine_loop<KK, PB>(B, list_a, count_a, list_b, count_b, cap_list, cap, fin_ins, ticket, runs_total, prefetch, bar,
+                        parity);
 }
 
 // Entry builder for the small-n path (one finish over the whole input).

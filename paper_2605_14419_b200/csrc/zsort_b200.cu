@@ -452,23 +452,43 @@ constexpr int TICK_SLOT[4] = {C_FTICK0, C_FTICK1, C_FTICK2, C_FTICK3};
 // Finish over `list`: count from device memory (count_dev, clamped to
 // count_const; persistent CTAs with a work ticket) or the host constant
 // count_const (one run per CTA); refine runs go to refine list `ref_out`.
+// With `fuse_par` >= 0 the launch is cooperative and the same grid then runs
+// the refine iterations of level parity `fuse_par` (no second launch).
 template <int KK, int PB>
 int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev, int64_t count_const,
-                  int64_t count_bound, int ref_out, int tick) {
+                  int64_t count_bound, int ref_out, int tick, int fuse_par = -1) {
     if (count_bound <= 0) return ZSB_OK;
     FinLayout FL = fin_layout((int)c.P.cap, PB);
     smem_optin(k_finish<KK, PB>, FL.total);
     Entry *refine = (Entry *)(c.ws + c.L.refine[ref_out]);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     const int64_t grid = count_dev ? std::min<int64_t>(count_bound, (int64_t)num_sms()) : count_bound;
+    RefineArgs ra{};
+    if (fuse_par >= 0) {
+        ra.list_b = (Entry *)(c.ws + c.L.refine[2 * fuse_par + 1]);
+        ra.count_b = ctrl + REF_SLOT[2 * fuse_par + 1];
+        ra.cap_list = c.L.ref_cap;
+        ra.ticket_b = ctrl + TICK_SLOT[2 * fuse_par + 1];
+        ra.runs_total = ctrl + C_ST_INSERTION;
+    }
     {
         PhaseScope ph(PH_FINISH, c.st);
-        k_finish<KK, PB><<<(unsigned)grid, FT, FL.total, c.st>>>(c.B, list, count_dev, count_const, (int)c.P.cap, refine,
-                                                                ctrl + REF_SLOT[ref_out],
-                                                                FIN_INS,  // refine lists hold <= n / (FIN_INS + 1) runs
-                                                                fin_prof(count_bound),
-                                                                count_dev ? ctrl + TICK_SLOT[tick] : nullptr,
-                                                                fin_prefetch(c.n, PB));
+        Buffers Bv = c.B;
+        const Entry *lst = list;
+        const unsigned long long *cd = count_dev;
+        int64_t cc = count_const;
+        int cap = (int)c.P.cap, fi = FIN_INS;  // refine lists hold <= n / (FIN_INS + 1) runs
+        long long *prof = fin_prof(count_bound);
+        unsigned long long *rc = ctrl + REF_SLOT[ref_out];
+        unsigned long long *tk = count_dev ? ctrl + TICK_SLOT[tick] : nullptr;
+        int pf = fin_prefetch(c.n, PB);
+        void *args[] = {&Bv, &lst, &cd, &cc, &cap, &refine, &rc, &fi, &prof, &tk, &pf, &ra};
+        if (fuse_par >= 0)
+            ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_finish<KK, PB>, dim3((unsigned)grid), dim3(FT), args,
+                                                 FL.total, c.st));
+        else
+            ZSB_CUDA(cudaLaunchKernel((const void *)k_finish<KK, PB>, dim3((unsigned)grid), dim3(FT), args, FL.total,
+                                      c.st));
     }
     ZSB_LAUNCH("k_finish");
     return ZSB_OK;
@@ -556,9 +576,12 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
                               int64_t bound, int par, bool zeroed = false) -> int {
         if (!zeroed) ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[2 * par], 0, 32, c.st));  // two counts, two tickets
-        int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par);
-        if (rc) return rc;
-        return launch_refine<KK, PB>(c, par);
+        if (env_int("ZSB_REFINE_LAUNCH", 0)) {  // the refine iterations as a launch of their own
+            int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par);
+            if (rc) return rc;
+            return launch_refine<KK, PB>(c, par);
+        }
+        return launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par, par);
     };
     // The sort is stream-ordered: once its last level is enqueued the call
     // returns, unless the caller asked for SortStats (or phase timing is on),
