@@ -681,7 +681,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             PhaseScope ph(PH_CLASSIFY, g_hs.side);
             const int64_t need = std::max<int64_t>(1, (std::max(total_slots, total_windows) + 1023) / 1024);
             const int cgrid = (int)std::min<int64_t>(need, (int64_t)num_sms());
-            int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = MIN_TILE;
+            int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = env_int("ZSB_MIN_TILE", MIN_TILE);
             int64_t ts = total_slots, tw = total_windows;
             Buffers Bv = c.B;
             unsigned long long *ref_zero = ctrl + REF_SLOT[2 * par];
