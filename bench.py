@@ -361,7 +361,7 @@ def roofline_from_phases(n, rec, ms_phase, launches, steps):
             "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
             "launch_ms": ms, "launches_per_step": phase_launch[dominant],
             "note": "alg bytes = 2 x (8 + payload) per key for the phase; time = the phase's CUDA-event time "
-                    "(main launch + refine pass); DRAM traffic per launch in profiles/"}
+                    "(finish and its refine iterations: one cooperative launch); DRAM traffic per launch in profiles/"}
     return roof, phase_ms
 
 
