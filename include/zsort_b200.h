@@ -17,8 +17,13 @@
  *  - inputs are never modified (core.py:351-352);
  *  - outputs and workspace are caller-allocated; kernels never allocate
  *    (_kernels.py:3-5);
- *  - no global mutable state: calls on different streams/workspaces are
- *    independent (reentrant);
+ *  - reentrant: a call's state lives in its workspace;
+ *    the library keeps only per-host-thread state (a pinned control-block
+ *    mirror, two events and a side stream per thread, created at first use)
+ *    and a once-per-device shared-memory opt-in guarded by a mutex, so
+ *    concurrent calls from different host threads on their own streams and
+ *    workspaces are independent (tests/test_gpu_parity.py::TestConcurrency);
+ *    nothing reads the environment (tuning constants are compile-time);
  *  - return 0 on success or a ZSB_ERR_* code; zsb_last_error() gives a
  *    thread-local message.  The Python wrapper maps ZSB_ERR_ARG/ZSB_ERR_NAN
  *    to ValueError and ZSB_ERR_DTYPE to TypeError, like core.py:151-181.
@@ -90,6 +95,21 @@ size_t zsb_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, 
 int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
              void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
              int64_t *h_stats, void *stream);
+
+/* zsort_rec (core.py:403-437 -> _kernels.zsort_rec_driver, _kernels.py:453-473):
+ * stable sort of one segment in the recursion phase, given the caller's
+ * bucket count k (clamped to one pass's fan-out, 2048), scale and estimated
+ * mean.  The segment starts at level depth + 1: one fused pass gathers min,
+ * max and the squared deviation around mean_est (_kernels.py:74-88), then
+ * Eq. 1 with (mean_est, std, zmin = |min - mean_est| / std, scale) buckets it;
+ * deeper levels size k to their segments like zsb_sort.  Validation as
+ * core.py:416-424: depth >= 1, k >= 2, scale > 0, n > insertion_threshold
+ * (ZSB_ERR_ARG).  Workspace: zsb_rec_workspace_bytes. */
+size_t zsb_rec_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, int64_t k);
+int zsb_sort_rec(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes,
+                 void *d_out_keys, void *d_out_payload, int64_t n, int64_t k, double scale, double mean_est,
+                 int64_t depth, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes, int64_t *h_stats,
+                 void *stream);
 
 /* Grid-wide moments of n keys (north-star subsystem 1; replaces
  * first_pass + variance_pass, _kernels.py:28-71, core.py:184-234).

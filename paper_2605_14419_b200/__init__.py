@@ -22,14 +22,19 @@ from .core import (  # noqa: F401
     check_stable_permutation_device,
     cluster_count,
     estimated_mean,
+    counting_sort_stable,
+    fallback_sort_stable,
     first_pass,
+    insertion_sort_stable,
     map_to_cluster,
     stable_scatter,
     zsort,
+    zsort_rec,
 )
 
 __all__ = [
     "DegenerateSpreadError", "FirstPassStats", "MappingParams", "PartitionPlan", "SortConfig", "SortStats",
     "all_equal", "build_mapping_params", "build_partition_plan", "check_stable_permutation_device",
-    "cluster_count", "estimated_mean", "first_pass", "map_to_cluster", "stable_scatter", "zsort",
+    "cluster_count", "counting_sort_stable", "estimated_mean", "fallback_sort_stable", "first_pass",
+    "insertion_sort_stable", "map_to_cluster", "stable_scatter", "zsort", "zsort_rec",
 ]

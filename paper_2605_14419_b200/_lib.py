@@ -34,7 +34,7 @@ ZSB_OK, ZSB_ERR_ARG, ZSB_ERR_DTYPE, ZSB_ERR_NAN, ZSB_ERR_WORKSPACE, ZSB_ERR_CUDA
 
 # Every symbol declared in include/zsort_b200.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "zsb_workspace_bytes", "zsb_sort", "zsb_moments", "zsb_histogram", "zsb_scatter",
+    "zsb_workspace_bytes", "zsb_sort", "zsb_rec_workspace_bytes", "zsb_sort_rec", "zsb_moments", "zsb_histogram", "zsb_scatter",
     "zsb_check_workspace_bytes", "zsb_check_sorted", "zsb_last_error", "zsb_version",
     "zsb_timing_enable", "zsb_timing_read",
     "zsb_local_moments", "zsb_bucket_histogram", "zsb_bucket_minmax", "zsb_partition_workspace_bytes",
@@ -66,6 +66,11 @@ def load(auto_build: bool = True):
     L.zsb_workspace_bytes.restype = SZ
     L.zsb_sort.argtypes = [P, I32, P, I32, P, P, I64, ctypes.POINTER(ZsbConfig), P, SZ, P, P]
     L.zsb_sort.restype = ctypes.c_int
+    L.zsb_rec_workspace_bytes.argtypes = [I64, I32, I32, I64]
+    L.zsb_rec_workspace_bytes.restype = SZ
+    L.zsb_sort_rec.argtypes = [P, I32, P, I32, P, P, I64, I64, ctypes.c_double, ctypes.c_double, I64,
+                               ctypes.POINTER(ZsbConfig), P, SZ, P, P]
+    L.zsb_sort_rec.restype = ctypes.c_int
     L.zsb_moments.argtypes = [P, I32, I64, P, SZ, P, P, P, P]
     L.zsb_moments.restype = ctypes.c_int
     L.zsb_histogram.argtypes = [P, I32, I64, P, I64, P, P, SZ, P]

@@ -33,7 +33,8 @@ from . import _lib
 __all__ = [
     "DegenerateSpreadError", "FirstPassStats", "MappingParams", "PartitionPlan", "SortConfig", "SortStats",
     "all_equal", "build_mapping_params", "build_partition_plan", "cluster_count", "estimated_mean",
-    "first_pass", "map_to_cluster", "stable_scatter", "zsort", "check_stable_permutation_device",
+    "first_pass", "map_to_cluster", "stable_scatter", "zsort", "zsort_rec", "insertion_sort_stable",
+    "counting_sort_stable", "fallback_sort_stable", "check_stable_permutation_device",
 ]
 
 INT64_MIN = -(2**63)
@@ -206,6 +207,38 @@ def zsort(keys, payload=None, config: SortConfig | None = None, *, out=None):
     ``out=(keys_out, payload_out)`` (torch tensors, e.g. pinned host buffers)
     receives the result instead of fresh allocations (extension).
     """
+    return _sort(keys, payload, config, out=out)
+
+
+def zsort_rec(keys, k: int, scale: float, mean_est: float, depth: int = 1, payload=None,
+              config: SortConfig | None = None):
+    """Recursive-phase sort of one segment given an estimated mean
+    (core.py:403-437 -> _kernels.zsort_rec_driver, _kernels.py:453-473).
+
+    Same validation as the reference (depth >= 1, k >= 2, scale > 0, more
+    records than the insertion threshold).  On the device the segment starts
+    at level depth + 1: one fused pass gathers min, max and the squared
+    deviation around ``mean_est`` and Eq. 1 buckets it with the caller's k
+    (clamped to one pass's fan-out, 2048) and scale; deeper levels size k to
+    their segments.  Returns ``(keys, payload, stats)``; the sorted output is
+    the unique stable order, identical to the reference's.
+    """
+    cfg = config if config is not None else SortConfig()
+    if depth < 1:
+        raise ValueError("depth must be >= 1")
+    if k < 2:
+        raise ValueError("k must be >= 2")
+    if not (scale > 0):
+        raise ValueError("scale must be positive")
+    kt, _ = _coerce_keys(keys)
+    if kt.numel() <= cfg.insertion_threshold:
+        raise ValueError("zsort_rec requires a segment larger than the insertion threshold")
+    if not math.isfinite(float(mean_est)):
+        raise ValueError("mean_est must be finite")
+    return _sort(keys, payload, cfg, rec=(int(k), float(scale), float(mean_est), int(depth)))
+
+
+def _sort(keys, payload=None, config: SortConfig | None = None, *, out=None, rec=None):
     cfg = config if config is not None else SortConfig()
     kt, kind = _coerce_keys(keys)
     n = kt.numel()
@@ -251,12 +284,20 @@ def zsort(keys, payload=None, config: SortConfig | None = None, *, out=None):
         out_k = torch.empty_like(d_keys)
         out_p = torch.empty_like(d_pay) if d_pay is not None else None
         c = cfg.to_c()
-        ws_bytes = L.zsb_workspace_bytes(n, kd, pb, c)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         stats = (_ctypes.c_int64 * 5)()
-        rc = L.zsb_sort(d_keys.data_ptr(), kd, d_pay.data_ptr() if d_pay is not None else None, pb,
-                        out_k.data_ptr(), out_p.data_ptr() if out_p is not None else None, n, c,
-                        ws.data_ptr(), ws_bytes, stats, _stream_ptr(dev))
+        dp_ptr = d_pay.data_ptr() if d_pay is not None else None
+        op_ptr = out_p.data_ptr() if out_p is not None else None
+        if rec is None:
+            ws_bytes = L.zsb_workspace_bytes(n, kd, pb, c)
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+            rc = L.zsb_sort(d_keys.data_ptr(), kd, dp_ptr, pb, out_k.data_ptr(), op_ptr, n, c,
+                            ws.data_ptr(), ws_bytes, stats, _stream_ptr(dev))
+        else:
+            rk, rscale, rmean, rdepth = rec
+            ws_bytes = L.zsb_rec_workspace_bytes(n, kd, pb, rk)
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+            rc = L.zsb_sort_rec(d_keys.data_ptr(), kd, dp_ptr, pb, out_k.data_ptr(), op_ptr, n, rk, rscale, rmean,
+                                rdepth, c, ws.data_ptr(), ws_bytes, stats, _stream_ptr(dev))
         _lib.check(rc)
         st = SortStats(*[int(x) for x in stats])
         if out is not None and kind == "torch" and gather_src is None:
@@ -285,6 +326,45 @@ def zsort(keys, payload=None, config: SortConfig | None = None, *, out=None):
 
 
 # ------------------------------------------------------- building blocks
+
+def insertion_sort_stable(keys, payload=None):
+    """core.py:288-296.  On the GPU every segment of at most the finish
+    capacity is one shared-memory finish run (rank by (key, index)); longer
+    inputs take the full partition pipeline.  Returns ``(keys, payload)``."""
+    k, p, _ = _sort(keys, payload)
+    return k, p
+
+
+def counting_sort_stable(keys, min_key: int, max_key: int, payload=None,
+                         range_threshold: int = SortConfig.counting_range_threshold):
+    """core.py:299-323: the exact range [min_key, max_key] is validated with
+    Python integers (span < 0, span >= range_threshold, keys outside the
+    range: ValueError); the keys' min/max come from the K1 moments kernel.
+    The finish's direct-digit mode is the GPU counting sort (one digit per
+    key value when the range fits its sub-buckets).  Returns ``(keys, payload)``."""
+    kt, _ = _coerce_keys(keys)
+    if kt.dtype != torch.int64:
+        raise TypeError("counting_sort_stable is defined for integer keys")
+    span = int(max_key) - int(min_key)
+    if span < 0:
+        raise ValueError("max_key must be >= min_key")
+    if span >= range_threshold:
+        raise ValueError(f"key range {span} is not below the counting threshold {range_threshold}")
+    if kt.numel():
+        st = first_pass(kt)
+        if st.min_key < int(min_key) or st.max_key > int(max_key):
+            raise ValueError("keys fall outside [min_key, max_key]")
+    k, p, _ = _sort(keys, payload)
+    return k, p
+
+
+def fallback_sort_stable(keys, payload=None):
+    """core.py:326-335 (the reference's merge-sort termination path).  On the
+    GPU termination is the exact MSD digit split inside the same pipeline
+    (K7), so this is the full stable sort.  Returns ``(keys, payload)``."""
+    k, p, _ = _sort(keys, payload)
+    return k, p
+
 
 def _moments(keys):
     kt, _ = _coerce_keys(keys)

@@ -12,6 +12,8 @@
 namespace zsb {
 
 constexpr uint64_t SIGN = 0x8000000000000000ull;
+constexpr uint64_t ORD_PINF = 0xFFF0000000000000ull;  // ord_key<KEY_F64>(+inf); positive NaNs order above
+constexpr uint64_t ORD_NINF = 0x000FFFFFFFFFFFFFull;  // ord_key<KEY_F64>(-inf); negative NaNs order below
 constexpr int WARP = 32;
 
 enum KeyKind { KEY_I64 = 0, KEY_F64 = 1 };
@@ -299,6 +301,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // Order earlier generic-proxy shared-memory accesses before async-proxy (TMA) writes.
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Order this thread's earlier generic-proxy global stores before later
+// async-proxy (TMA bulk copy) reads of the same data by any thread that
+// synchronises with it afterwards (PTX memory model, proxy fences).
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
 // One TMA bulk copy global -> shared (16-byte aligned addresses, size a multiple of 16).

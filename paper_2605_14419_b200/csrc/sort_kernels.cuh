@@ -38,6 +38,7 @@ struct Buffers {
     void *out_p;
     const DestCuts *cuts;  // MODE_DEST only
     const float2 *cdf;     // MODE_ZCDF only: kf knot pairs (cdf[s], cdf[s+1]) in bucket units (staged in smem)
+    unsigned long long *status;  // ZSB_ERR_NAN is raised here by a finish run holding a NaN (nullable)
 };
 
 __device__ __forceinline__ const uint64_t *src_keys(const Buffers &B, int src) {
@@ -127,6 +128,9 @@ __device__ inline double exact_mean(long long sum_hi, unsigned long long sum_lo,
 struct MapCfg {
     int32_t mapping;      // 0 fitted, 1 paper
     int32_t depth_guard;  // levels before the exact integer split
+    int32_t scale_level;  // paper mode: segments at this level take `scale` (zsort_rec's given scale); 0: none
+    int32_t pad;
+    double scale;
 };
 
 // Decide the mapping of one segment from its center, variance and exact
@@ -146,7 +150,7 @@ __device__ void finalize_params(SegParams &p, double var, uint64_t omin, uint64_
     if (ok) {
         if (mc.mapping == 1) {  // paper Eq. 1: zmin = |min - mean| / std, scale = k / 4
             p.zmin = fabs(__ddiv_rn(__dsub_rn(vmin, p.center), sd));
-            p.scale = (double)p.k / 4.0;
+            p.scale = (mc.scale_level && p.level == mc.scale_level) ? mc.scale : (double)p.k / 4.0;
         } else {  // fitted: min -> 0, max -> just below k
             double span = __ddiv_rn(__dsub_rn(vmax, vmin), sd);
             ok = (span > 0.0) && isfinite(span);
@@ -698,8 +702,7 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
 
 template <int KK, int PB, int SW, int BM>
 __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *__restrict__ segs, int nseg,
-                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof,
-                                             int tie_check) {
+                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof) {
 #ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
     long long t_mark = prof ? clock64() : 0;
     long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
@@ -806,11 +809,18 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             const int q = w * k + (bkj < 0 ? 0 : bkj);
             const uint32_t sh = 16 * (q & 1);
             uint32_t *word = (uint32_t *)cnt + (q >> 1);
+            // the warp executes the atomic as one instruction and re-reads its
+            // counters after it (converged: __syncwarp here, __any_sync below),
+            // so a tie group of g lanes finds after == group start + g
+            __syncwarp();
             if (bkj >= 0) {
                 old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
-                if (tie_check) after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
+                after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
             }
-            if (tie_check) {
+            {
+                // a tie group (lanes of this instruction sharing a bucket) is
+                // re-ranked in lane order whatever order the hardware handed
+                // out the old values in: stable by construction
                 const bool tie = bkj >= 0 && after != old + 1u;
                 if (__any_sync(0xffffffffu, tie)) {
                     const unsigned m = __match_any_sync(0xffffffffu, bkj);
@@ -885,38 +895,11 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
 template <int KK, int PB, int SW>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
-                                                              int dst_sel, long long *prof, int tie_check) {
+                                                              int dst_sel, long long *prof) {
     if (segs[find_seg(segs, nseg, blockIdx.x)].mode == MODE_ZCDF)
-        scatter_body<KK, PB, SW, 1>(B, segs, nseg, mat, dst_sel, prof, tie_check);
+        scatter_body<KK, PB, SW, 1>(B, segs, nseg, mat, dst_sel, prof);
     else
-        scatter_body<KK, PB, SW, 0>(B, segs, nseg, mat, dst_sel, prof, tie_check);
-}
-
-// Probe (once per device, at first use): do the lanes of one warp that hit
-// the same shared-memory word with atomicAdd receive their old values in lane
-// order?  sm_100 does (0 violations in millions of tie groups), and then
-// k_scatter skips its tie detection; any violation keeps it on.
-__global__ void k_probe_atomic_order(const uint32_t seed, unsigned long long *viol) {
-    __shared__ uint32_t cnt[1024];
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) cnt[i] = 0;
-    __syncthreads();
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-    unsigned long long v = 0;
-    uint32_t r = seed ^ (threadIdx.x * 0x9E3779B9u);
-    for (int it = 0; it < 256; it++) {
-        r = r * 1664525u + 1013904223u;
-        const int nb = 2 << (it & 5);  // 2 .. 64 buckets
-        const int b = (int)((r >> 8) % (uint32_t)nb);
-        const int q = w * 64 + b;  // per-(warp, bucket) u16 counter, two per word
-        const uint32_t sh = 16 * (q & 1);
-        const uint32_t old = (atomicAdd(&cnt[q >> 1], 1u << sh) >> sh) & 0xFFFFu;
-        const unsigned m = __match_any_sync(0xffffffffu, b);
-        for (int l = 0; l < 32; l++) {
-            const uint32_t o2 = __shfl_sync(0xffffffffu, old, l);
-            v += ((m >> l) & 1u) && l < lane && o2 > old;
-        }
-    }
-    if (v) atomicAdd(viol, v);
+        scatter_body<KK, PB, SW, 0>(B, segs, nseg, mat, dst_sel, prof);
 }
 
 // ------------------------------------------------------- equalisation
@@ -1820,6 +1803,11 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
     }
     omin = warp_min_u64(lane < FW ? r_min[lane] : ~0ull);  // every warp reduces the warp partials itself
     omax = warp_max_u64(lane < FW ? r_max[lane] : 0ull);
+    if constexpr (KK == KEY_F64) {
+        // NaNs order outside [-inf, +inf] in the ordered image: a run holding
+        // one raises ZSB_ERR_NAN (the small-n path reaches no other screen)
+        if (tid == 0 && B.status && (omax > ORD_PINF || omin < ORD_NINF)) *B.status = 3ull;
+    }
     auto key_bits = [&](uint64_t ov, int idx) -> uint64_t {
         uint64_t kb = key_from_ord<KK>(ov);
         if (KK == KEY_F64 && anyneg && ((negzero[idx >> 5] >> (idx & 31)) & 1u)) kb = SIGN;
@@ -2203,6 +2191,9 @@ __device__ void refine_loop(const Buffers &B, Entry *list_a, unsigned long long 
         if (ne == 0) break;  // every CTA reads the same value (written before the last grid barrier)
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(runs_total, (unsigned long long)ne);
         finish_list<KK, PB>(B, lin, ne, cap, lout, cout, fin_ins, nullptr, ticket, prefetch, bar, parity);
+        // the next pass stages this pass's generic-proxy output stores with
+        // TMA bulk copies (async proxy): fence them before the grid barrier
+        fence_proxy_async_global();
         grid.sync();  // pass done: its refine runs are all in lout
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             *cin = 0ull;
@@ -2252,6 +2243,7 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
         finish_list<KK, PB>(B, entries, ne, cap, refine, refine_count, fin_ins, prof, ticket, prefetch, bar, parity);
     }
     if (ra.list_b) {
+        fence_proxy_async_global();  // refine runs are re-staged by TMA (async proxy) after the barrier
         cg::this_grid().sync();  // every refine run of the list is published
         refine_loop<KK, PB>(B, refine, refine_count, ra.list_b, ra.count_b, ra.cap_list, cap, fin_ins, ra.ticket_b,
                             ra.runs_total, prefetch, bar, parity);

@@ -105,10 +105,42 @@ void timing_collect() {
         if (e_ != cudaSuccess) return fail(ZSB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
+// Tuning constants: the defaults are the measured best on B200 (DESIGN.md
+// §4, knob table); experiments rebuild the library with -D<NAME>=<value>
+// (tools/build_variant.sh).  Nothing in the library reads the environment.
+#ifndef ZSB_K1MAX
+#define ZSB_K1MAX 1024  // cap on the fitted level-1 bucket count
+#endif
+#ifndef ZSB_SW16_ABOVE
+#define ZSB_SW16_ABOVE 512  // bucket counts above this use 16-warp, 8192-record scatter rounds
+#endif
+#ifndef ZSB_TILES_PER_SM
+#define ZSB_TILES_PER_SM 0  // level-1 tiles per SM; 0: 1 for 16-warp scatter rounds, 2 for 8-warp
+#endif
+#ifndef ZSB_WIN_PCT
+#define ZSB_WIN_PCT 75  // level-1 finish window, % of the run capacity
+#endif
+#ifndef ZSB_CHILD_FILL
+#define ZSB_CHILD_FILL 2  // recursion children: k = pow2 >= fill * len / cap
+#endif
+#ifndef ZSB_GREEDY
+#define ZSB_GREEDY 1  // greedy finish runs on recursion levels (else fixed windows)
+#endif
+#ifndef ZSB_MIN_TILE
+#define ZSB_MIN_TILE 8192  // recursion tile floor (raised up to 4x on long levels)
+#endif
+#ifndef ZSB_L2_PREFETCH
+#define ZSB_L2_PREFETCH -1  // L2 prefetch of each CTA's next finish run: -1 auto (records > 128 MB), 0/1 forced
+#endif
+#ifndef ZSB_NO_SAMPLE
+#define ZSB_NO_SAMPLE 0  // 1: exact K1 + exact coarse histogram at level 1 instead of the sample
+#endif
+#ifndef ZSB_NO_EQUALIZE
+#define ZSB_NO_EQUALIZE 0  // 1: plain fitted z-score at level 1 (no CDF equalisation)
+#endif
+#ifndef ZSB_REFINE_LAUNCH
+#define ZSB_REFINE_LAUNCH 0  // 1: refine iterations as a launch of their own instead of inside the finish grid
+#endif
 
 int num_sms() {
     static int sms = 0;
@@ -123,7 +155,6 @@ int num_sms() {
 
 constexpr int K_LEVEL1_MAX = KSCAT_MAX;  // fan-out of one scatter pass
 constexpr int KMAX_CHILD = 1024;
-constexpr int MIN_TILE = 8192;  // recursion tile floor (k_plan raises it on long levels)
 
 int finish_cap(int pb) { return FT * (pb == 8 ? FinItems<8>::F : (pb == 4 ? FinItems<4>::F : FinItems<0>::F)); }
 
@@ -133,8 +164,7 @@ int finish_cap(int pb) { return FT * (pb == 8 ? FinItems<8>::F : (pb == 4 ? FinI
 // wider window packs small buckets into fuller runs (fewer, longer finish
 // runs); measured on B200 (C4): 50% 4.80 ms, 66% 4.52 ms, 75% 4.43 ms.
 int64_t fin_window(int64_t cap) {
-    const int pct = env_int("ZSB_WIN_PCT", 75);
-    return std::max<int64_t>(256, std::min<int64_t>(cap - 256, cap * pct / 100));
+    return std::max<int64_t>(256, std::min<int64_t>(cap - 256, cap * ZSB_WIN_PCT / 100));
 }
 
 int64_t cluster_count(int64_t n, double alpha) {  // core.py:146-148
@@ -161,13 +191,25 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
     if (cfg.mapping == ZSB_MAP_PAPER) {
         P.k = std::min<int64_t>(cluster_count(n, cfg.alpha), K_LEVEL1_MAX);
     } else {
-        int64_t kmax = env_int("ZSB_K1MAX", 1024);  // runs of >= 4 records per 4096-record round
+        const int64_t kmax = ZSB_K1MAX;  // runs of >= 4 records per 4096-record round
         P.k = std::min<int64_t>(std::max<int64_t>(16, pow2_at_least((4 * n + P.cap - 1) / P.cap)), kmax);
     }
-    int64_t target_tiles =
-        (int64_t)num_sms() * env_int("ZSB_TILES_PER_SM", scat_warps((int)P.k, env_int("ZSB_SW16_ABOVE", 512)) == 8 ? 2 : 1);
+    const int tps = ZSB_TILES_PER_SM > 0 ? ZSB_TILES_PER_SM : (scat_warps((int)P.k, ZSB_SW16_ABOVE) == 8 ? 2 : 1);
+    int64_t target_tiles = (int64_t)num_sms() * tps;
     int64_t tl = std::max<int64_t>(4 * P.k, (n + target_tiles - 1) / target_tiles);
     tl = std::max<int64_t>(tl, 2048);
+    tl = (tl + 255) & ~(int64_t)255;
+    P.tile_len = tl;
+    P.ntiles = (n + tl - 1) / tl;
+    return P;
+}
+
+// zsort_rec plan: the caller's k (clamped to one pass's fan-out), level-1 tiling.
+Plan1 plan_rec(int64_t n, int pb, int64_t k) {
+    zsb_config c = zsb_config{0.6, 96, 65000, 32, 0, ZSB_MAP_PAPER};
+    Plan1 P = plan_level1(n, pb, c);
+    P.k = std::max<int64_t>(2, std::min<int64_t>(k, K_LEVEL1_MAX));
+    int64_t tl = std::max<int64_t>(std::max<int64_t>(4 * P.k, 2048), P.tile_len);
     tl = (tl + 255) & ~(int64_t)255;
     P.tile_len = tl;
     P.ntiles = (n + tl - 1) / tl;
@@ -258,7 +300,7 @@ void smem_optin(F *func, size_t bytes) {
 
 __global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t *wfirst, int64_t nwin, int64_t n, int64_t k,
                               int64_t tile_len, int64_t ntiles, int src, double center, double sd, double zmin,
-                              double scale, int mode) {
+                              double scale, int mode, int level = 1) {
     SegParams p{};
     p.center = center;
     p.std = sd;
@@ -273,7 +315,7 @@ __global__ void k_init_level1(SegParams *seg, int64_t *kfirst, int64_t *wfirst, 
     p.k = (int32_t)k;
     p.ntiles = (int32_t)ntiles;
     p.mode = mode;
-    p.level = 1;
+    p.level = level;
     p.src = src;
     *seg = p;
     kfirst[0] = 0;
@@ -301,10 +343,13 @@ struct Ctx {
     int64_t n;
 };
 
+#ifdef ZSB_PHASE_PROFILE
+// Instrumentation build only (-DZSB_PHASE_PROFILE): per-CTA clock64 phase
+// profiles of the scatter and the largest finish launch, dumped to stderr.
 long long *g_scat_prof = nullptr;
 int64_t g_scat_prof_n = 0;
 long long *scat_prof(int64_t n) {
-    if (!env_int("ZSB_FIN_PROFILE", 0) || n < g_scat_prof_n) return nullptr;
+    if (n < g_scat_prof_n) return nullptr;
     if (g_scat_prof) cudaFree(g_scat_prof);
     cudaMalloc(&g_scat_prof, (size_t)n * 8 * 8);
     cudaMemset(g_scat_prof, 0, (size_t)n * 8 * 8);
@@ -326,33 +371,9 @@ void scat_prof_dump() {
     g_scat_prof = nullptr;
     g_scat_prof_n = 0;
 }
-
-// 1 if the scatter must detect same-bucket lanes of one atomic instruction
-// (shared atomics not handed out in lane order on this device); probed once
-// per device.  ZSB_TIE_CHECK=0/1 overrides.
-int scatter_tie_check() {
-    static int dev_flag[64];
-    static bool probed[64] = {false};
-    static std::mutex mu;
-    const int forced = env_int("ZSB_TIE_CHECK", -1);
-    if (forced >= 0) return forced ? 1 : 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return 1;
-    std::lock_guard<std::mutex> g(mu);
-    if (!probed[dev]) {
-        unsigned long long *d = nullptr, h = 1;
-        if (cudaMalloc(&d, 8) == cudaSuccess) {
-            cudaMemset(d, 0, 8);
-            k_probe_atomic_order<<<8, 512>>>(0x1234567u, d);
-            if (cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost) != cudaSuccess) h = 1;
-            cudaFree(d);
-        }
-        dev_flag[dev] = h ? 1 : 0;
-        probed[dev] = true;
-    }
-    return dev_flag[dev];
-}
+#else
+inline long long *scat_prof(int64_t) { return nullptr; }
+#endif
 
 // L2 prefetch of the next finish run by the copy engine: only when the
 // level's records exceed the L2; below it the scatter's evict_last runs are
@@ -360,8 +381,7 @@ int scatter_tie_check() {
 // +5 us, C4 -47 us).  (The same prefetch of the scatter's next round of keys
 // won 1 % at C4/X9 but cost C2 its register allocation: not used.)
 int fin_prefetch(int64_t n, int pb) {
-    const int forced = env_int("ZSB_L2_PREFETCH", -1);
-    if (forced >= 0) return forced;
+    if (ZSB_L2_PREFETCH >= 0) return ZSB_L2_PREFETCH;
     return (double)n * (8 + pb) > 128.0 * (1 << 20) ? 1 : 0;
 }
 
@@ -390,31 +410,28 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     ZSB_LAUNCH("k_scan");
     if (after_scan) ZSB_CUDA(cudaEventRecord(after_scan, c.st));
     const size_t cdf_bytes = (c.B.cdf && segs_level1) ? (size_t)(CDF_KNOTS + 1) * 8 : 0;
-    const bool sw16 = scat_warps(kmax, env_int("ZSB_SW16_ABOVE", 512)) == 16 &&
+    const bool sw16 = scat_warps(kmax, ZSB_SW16_ABOVE) == 16 &&
                       scat_layout(kmax, PB, 16).total + cdf_bytes <= (size_t)227 * 1024 - 1024;
     if (!sw16) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 8>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 8><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles),
-                                                                    scatter_tie_check());
+        k_scatter<KK, PB, 8><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
     } else {
         const size_t sbytes = scat_layout(kmax, PB, 16).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 16>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 16><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles),
-                                                                     scatter_tie_check());
+        k_scatter<KK, PB, 16><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
 }
 
-// ZSB_FIN_PROFILE=1: per-CTA phase timestamps of the largest finish launch
-// are dumped to stderr (instrumentation only).
+#ifdef ZSB_PHASE_PROFILE
 long long *g_fin_prof = nullptr;
 int64_t g_fin_prof_n = 0;
 long long *fin_prof(int64_t n) {
-    if (!env_int("ZSB_FIN_PROFILE", 0) || n <= g_fin_prof_n) return nullptr;  // first launch of the largest size
+    if (n <= g_fin_prof_n) return nullptr;  // first launch of the largest size
     if (g_fin_prof) cudaFree(g_fin_prof);
     cudaMalloc(&g_fin_prof, (size_t)n * 8 * 8);
     cudaMemset(g_fin_prof, 0, (size_t)n * 8 * 8);
@@ -442,6 +459,9 @@ void fin_prof_dump() {
     g_fin_prof = nullptr;
     g_fin_prof_n = 0;
 }
+#else
+inline long long *fin_prof(int64_t) { return nullptr; }
+#endif
 
 // Refine lists: two per level parity (a level's finish writes list 2*par,
 // its refine pass list 2*par + 1), so a level's leftovers survive the next
@@ -545,8 +565,17 @@ int host_sync_init() {
     return ZSB_OK;
 }
 
+// zsort_rec's start (core.py:403-437, _kernels.py:453-473): one segment at
+// level depth + 1 centred on the caller's estimated mean, bucketed with the
+// caller's k and scale (paper Eq. 1) at that first level.
+struct RecStart {
+    double center, scale;
+    int64_t k;
+    int32_t level;
+};
+
 template <int KK, int PB>
-int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
+int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *rec = nullptr) {
     const int64_t n = c.n;
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     SegParams *seg_cur = (SegParams *)(c.ws + c.L.seg_a);
@@ -560,8 +589,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int64_t stats[ZSB_STAT_SLOTS] = {0, 0, 0, 0, 0};
     if (int rc = host_sync_init()) return rc;
     unsigned long long *hc = g_hs.ctrl;  // pinned: the copies below are truly asynchronous
-    const bool fused_l1 = c.n > c.P.cap && cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0) &&
-                          !env_int("ZSB_NO_SAMPLE", 0);
+    const bool fused_l1 =
+        !rec && c.n > c.P.cap && cfg.mapping == ZSB_MAP_FITTED && !ZSB_NO_EQUALIZE && !ZSB_NO_SAMPLE;
     if (!fused_l1) ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));  // else k_level1_map clears it
     auto full_sync = [&]() -> int {  // control block -> host, wait for everything enqueued
         ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, c.st));
@@ -576,7 +605,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     auto enqueue_finish = [&](const Entry *list, const unsigned long long *count_dev, int64_t count_const,
                               int64_t bound, int par, bool zeroed = false) -> int {
         if (!zeroed) ZSB_CUDA(cudaMemsetAsync(ctrl + REF_SLOT[2 * par], 0, 32, c.st));  // two counts, two tickets
-        if (env_int("ZSB_REFINE_LAUNCH", 0)) {  // the refine iterations as a launch of their own
+        if (ZSB_REFINE_LAUNCH) {  // the refine iterations as a launch of their own
             int rc = launch_finish<KK, PB>(c, list, count_dev, count_const, bound, 2 * par, 2 * par);
             if (rc) return rc;
             return launch_refine<KK, PB>(c, par);
@@ -607,14 +636,19 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         int rc = enqueue_finish(entries, nullptr, 1, 1, 0);
         if (rc) return rc;
         stats[ZSB_STAT_INSERTION] = 1;
+        if (KK == KEY_F64) {  // the finish is this path's only NaN screen: wait for its verdict
+            if (int rs = full_sync()) return rs;
+            if (hc[C_STATUS] == 3) return fail(ZSB_ERR_NAN, "NaN keys have no order");
+        }
         return finish_call();
     }
 
-    MapCfg mc{cfg.mapping, (int32_t)cfg.depth_guard};
+    MapCfg mc{rec ? (int32_t)ZSB_MAP_PAPER : cfg.mapping, (int32_t)cfg.depth_guard, rec ? rec->level : 0, 0,
+              rec ? rec->scale : 0.0};
     ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping,
-                (int32_t)std::max(1, std::min(16, env_int("ZSB_CHILD_FILL", 2))), env_int("ZSB_GREEDY", 1)};
+                (int32_t)std::max(1, std::min(16, ZSB_CHILD_FILL)), ZSB_GREEDY};
     const int64_t nwin1 = (n + c.P.half - 1) / c.P.half;
-    const bool equalize = cfg.mapping == ZSB_MAP_FITTED && !env_int("ZSB_NO_EQUALIZE", 0);
+    const bool equalize = !rec && cfg.mapping == ZSB_MAP_FITTED && !ZSB_NO_EQUALIZE;
     unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
     float2 *cdf_tab = (float2 *)(c.ws + c.L.lut);
     if (fused_l1) {
@@ -630,6 +664,13 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                         &sparts, &mparts, &fine, &cdf_tab, &ctrl, &mc, &kf};
         PhaseScope ph(PH_MOMENTS, c.st);
         ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_level1_map<KK>, dim3(num_sms()), dim3(LT), args, 0, c.st));
+    } else if (rec) {
+        // the caller's centre; the fused stats pass of the loop's first
+        // iteration (k_seg_moments) gathers min, max and the squared
+        // deviation around it (_kernels.py:74-88, 453-473)
+        PhaseScope ph(PH_MISC, c.st);
+        k_init_level1<<<1, 1, 0, c.st>>>(seg_cur, kfirst, wfirst, nwin1, n, c.P.k, c.P.tile_len, c.P.ntiles, 0,
+                                         rec->center, 1.0, 0.0, 1.0, MODE_ZSCORE, rec->level);
     } else {
         {
             PhaseScope ph(PH_MISC, c.st);
@@ -660,8 +701,12 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
     int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
     int kmax = (int)c.P.k;
     int level = 1, par = 0;
+    if (rec) {  // the segment's own stats pass, then the level loop as for a recursion level
+        SegAcc a0{~0ull, 0ull, 0.0, 0.0};
+        ZSB_CUDA(cudaMemcpyAsync(acc, &a0, sizeof(a0), cudaMemcpyHostToDevice, c.st));
+    }
     while (true) {
-        if (level > 1) {
+        if (level > 1 || rec) {
             {
                 PhaseScope ph(PH_SEGSTATS, c.st, 2);
                 k_seg_moments<KK><<<(unsigned)tiles, NT, 0, c.st>>>(c.B, seg_cur, nseg, acc);
@@ -681,7 +726,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
             PhaseScope ph(PH_CLASSIFY, g_hs.side);
             const int64_t need = std::max<int64_t>(1, (std::max(total_slots, total_windows) + 1023) / 1024);
             const int cgrid = (int)std::min<int64_t>(need, (int64_t)num_sms());
-            int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = env_int("ZSB_MIN_TILE", MIN_TILE);
+            int nseg_ = nseg, key_kind = KK, kmc = KMAX_CHILD, mt = ZSB_MIN_TILE;
             int64_t ts = total_slots, tw = total_windows;
             Buffers Bv = c.B;
             unsigned long long *ref_zero = ctrl + REF_SLOT[2 * par];
@@ -710,7 +755,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         }
         stats[ZSB_STAT_INSERTION] += nentry;
         const int64_t nchild = (int64_t)hc[C_NCHILD];
-        if (env_int("ZSB_DEBUG", 0)) {  // host time since the call started: when this level's classify was seen
+#ifdef ZSB_DEBUG_LOG
+        {  // host time since the call started: when this level's classify was seen
             static thread_local std::chrono::steady_clock::time_point t_call;
             if (level == 1) t_call = std::chrono::steady_clock::now();
             const double us =
@@ -719,6 +765,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
                             " (host +%.0f us)\n",
                     level, nseg, (long long)tiles, kmax, (long long)nchild, (long long)nentry, hc[C_ST_FALLBACKS], us);
         }
+#endif
         if (nchild == 0) break;
         if (nchild > c.L.seg_cap) return fail(ZSB_ERR_WORKSPACE, "segment table overflow");
         nseg = (int)nchild;
@@ -734,10 +781,10 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats) {
         level++;
         if (level > 200) return fail(ZSB_ERR_CUDA, "partition did not terminate");
     }
-    if (env_int("ZSB_FIN_PROFILE", 0)) {
-        fin_prof_dump();
-        scat_prof_dump();
-    }
+#ifdef ZSB_PHASE_PROFILE
+    fin_prof_dump();
+    scat_prof_dump();
+#endif
     return finish_call();
 }
 
@@ -784,7 +831,9 @@ int dispatch(int kd, int pb, A &&...args) {
 
 template <int KK, int PB>
 struct SortOp {
-    static int run(Ctx &c, const zsb_config &cfg, int64_t *h_stats) { return run_sort<KK, PB>(c, cfg, h_stats); }
+    static int run(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *rec) {
+        return run_sort<KK, PB>(c, cfg, h_stats, rec);
+    }
 };
 
 // -------------------------------------------------------------- K8 check
@@ -842,6 +891,7 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = nullptr;
     ctx.B.cdf = nullptr;
+    ctx.B.status = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0],
@@ -929,9 +979,12 @@ size_t zsb_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, 
     return make_layout(n, payload_bytes, P, true).total;
 }
 
-int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
-             void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
-             int64_t *h_stats, void *stream) {
+}  // extern "C"
+
+namespace {
+int sort_entry(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
+               void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
+               int64_t *h_stats, void *stream, const RecStart *rec) {
     int rc = check_common(d_keys, key_dtype, payload_bytes, n);
     if (rc) return rc;
     zsb_config c = cfg ? *cfg : default_cfg();
@@ -943,7 +996,7 @@ int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32
         return fail(ZSB_ERR_ARG, "null output or payload pointer");
     Ctx ctx;
     ctx.n = n;
-    ctx.P = plan_level1(n, payload_bytes, c);
+    ctx.P = rec ? plan_rec(n, payload_bytes, rec->k) : plan_level1(n, payload_bytes, c);
     ctx.L = make_layout(n, payload_bytes, ctx.P, true);
     if (!d_workspace || workspace_bytes < ctx.L.total) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
     ctx.ws = (unsigned char *)d_workspace;
@@ -956,7 +1009,42 @@ int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = nullptr;
     ctx.B.cdf = (const float2 *)(ctx.ws + ctx.L.lut);
-    return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats);
+    ctx.B.status = (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS;
+    return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats, rec);
+}
+}  // namespace
+
+extern "C" {
+
+int zsb_sort(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, void *d_out_keys,
+             void *d_out_payload, int64_t n, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes,
+             int64_t *h_stats, void *stream) {
+    return sort_entry(d_keys, key_dtype, d_payload, payload_bytes, d_out_keys, d_out_payload, n, cfg, d_workspace,
+                      workspace_bytes, h_stats, stream, nullptr);
+}
+
+size_t zsb_rec_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, int64_t k) {
+    (void)key_dtype;
+    if (n < 1) n = 1;
+    return make_layout(n, payload_bytes, plan_rec(n, payload_bytes, k), true).total;
+}
+
+int zsb_sort_rec(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes,
+                 void *d_out_keys, void *d_out_payload, int64_t n, int64_t k, double scale, double mean_est,
+                 int64_t depth, const zsb_config *cfg, void *d_workspace, size_t workspace_bytes, int64_t *h_stats,
+                 void *stream) {
+    // core.py:416-424 validation
+    if (depth < 1) return fail(ZSB_ERR_ARG, "depth must be >= 1");
+    if (k < 2) return fail(ZSB_ERR_ARG, "k must be >= 2");
+    if (!(scale > 0.0)) return fail(ZSB_ERR_ARG, "scale must be positive");
+    if (!std::isfinite(mean_est)) return fail(ZSB_ERR_ARG, "mean_est must be finite");
+    zsb_config c = cfg ? *cfg : default_cfg();
+    if (n <= c.insertion_threshold && n > 0)
+        return fail(ZSB_ERR_ARG, "zsort_rec requires a segment larger than the insertion threshold");
+    if (depth + 1 > (int64_t)1 << 30) return fail(ZSB_ERR_ARG, "depth too large");
+    RecStart r{mean_est, scale, std::min<int64_t>(k, K_LEVEL1_MAX), (int32_t)(depth + 1)};
+    return sort_entry(d_keys, key_dtype, d_payload, payload_bytes, d_out_keys, d_out_payload, n, &c, d_workspace,
+                      workspace_bytes, h_stats, stream, &r);
 }
 
 int zsb_moments(const void *d_keys, int32_t key_dtype, int64_t n, void *d_workspace, size_t workspace_bytes,
@@ -1215,6 +1303,7 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ctx.B.out_p = d_out_payload;
     ctx.B.cuts = dc;
     ctx.B.cdf = nullptr;
+    ctx.B.status = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     count_launches(1);

@@ -367,17 +367,18 @@ def test_harness_seam(Z):
     assert r.verified and r.size == keys.size and r.min_ms > 0
 
 
-@pytest.mark.parametrize("tie_check", ["0", "1"])
-def test_scatter_tie_paths(Z, tie_check, monkeypatch):
+def test_scatter_tie_groups(Z):
     # the scatter ranks items with shared atomics; lanes of one instruction
-    # that share a bucket are either trusted to the device's lane order (probed
-    # at first use) or detected and re-ranked: both paths must be stable
-    monkeypatch.setenv("ZSB_TIE_CHECK", tie_check)
+    # that share a bucket (tie groups) are detected on every instruction and
+    # re-ranked in lane order, so stability does not rest on the hardware's
+    # order of atomic results
     rng = np.random.default_rng(77)
     few = rng.integers(0, 50, size=2_000_000).astype(np.int64)
     assert_matches_oracle(Z, few)
     runs = np.repeat(rng.standard_normal(20_000), 100)  # sorted-run-like ties inside warps
     assert_matches_oracle(Z, runs)
+    two = rng.integers(0, 2, size=3_000_000).astype(np.int64) << 40  # two buckets: every lane ties
+    assert_matches_oracle(Z, two)
 
 
 def _nested_scales(rng, n, levels, outliers=12):
