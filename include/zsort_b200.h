@@ -150,12 +150,33 @@ int zsb_check_sorted(const void *d_in_keys, const void *d_out_keys, const void *
  * between these calls from paper_2605_14419_b200/dist.py over
  * torch.distributed).  All are stream-ordered on `stream`. ---- */
 
-/* D1 payload: d_out3 = {count, sum(x - shift), sum((x - shift)^2)} (double)
- * and d_out_bits2 = ordered (order-preserving uint64) min and max of the
- * local shard; both are initialised by the call.  Replaces first_pass +
+/* D1 payload, one pass over the shard: d_out4 = {count, sum(x - c),
+ * sum((x - c)^2), c} (double) with c = shift, or the shard's first key when
+ * shift is NaN, and d_out_bits2 = ordered (order-preserving uint64) min and
+ * max of the local shard; both are initialised by the call.  The ranks
+ * combine the four values with Chan's merge.  Replaces first_pass +
  * variance_pass (_kernels.py:28-71) for a shard. */
-int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double shift, double *d_out3,
+int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double shift, double *d_out4,
                       uint64_t *d_out_bits2, void *stream);
+
+/* Index of the `occurrence`-th (0-based) local record whose key equals the
+ * key with bits key_bits (-0.0 and +0.0 are one key), or -1: the record a
+ * cut inside a one-valued run falls on.  Workspace of
+ * zsb_occurrence_workspace_bytes(); blocks until done. */
+size_t zsb_occurrence_workspace_bytes(void);
+
+/* Counter-based generator of the reference's key families on the device
+ * (datagen.py:92-162 shapes; gen_kernels.cuh): family 0 uniform, 1 normal,
+ * 2 skewed (Pareto), 3 nearly_sorted, 4 high_duplicate.  Writes the int64
+ * keys of global positions [offset, offset + n) of an n_total-key workload
+ * to d_out; key i depends only on (family, seed, i, params), so shards and
+ * checkers regenerate any key independently.  params (may be NULL for the
+ * reference defaults) = {normal_mu, normal_sigma, pareto_alpha, pareto_xm,
+ * swap_fraction, dup_range}.  Stream-ordered. */
+int zsb_generate(int32_t family, int64_t offset, int64_t n, int64_t n_total, uint64_t seed, const double *params,
+                 int64_t *d_out, void *stream);
+int zsb_occurrence_index(const void *d_keys, int32_t key_dtype, int64_t n, uint64_t key_bits, int64_t occurrence,
+                         void *d_workspace, int64_t *h_index, void *stream);
 
 /* D2 payload: histogram of the k global z-score buckets (params = {center,
  * std, zmin, scale}, Eq. 1, _kernels.py:91-112) into d_counts (int64[k],

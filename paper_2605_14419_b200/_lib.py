@@ -38,7 +38,8 @@ EXPORTS = (
     "zsb_check_workspace_bytes", "zsb_check_sorted", "zsb_last_error", "zsb_version",
     "zsb_timing_enable", "zsb_timing_read",
     "zsb_local_moments", "zsb_bucket_histogram", "zsb_bucket_minmax", "zsb_partition_workspace_bytes",
-    "zsb_partition_to_ranks", "zsb_range_histogram",
+    "zsb_partition_to_ranks", "zsb_range_histogram", "zsb_occurrence_workspace_bytes", "zsb_occurrence_index",
+    "zsb_generate",
 )
 
 PHASES = ("moments", "histogram", "scan", "scatter", "classify", "finish", "recursion_stats", "misc")
@@ -84,6 +85,12 @@ def load(auto_build: bool = True):
     D = ctypes.c_double
     L.zsb_local_moments.argtypes = [P, I32, I64, D, P, P, P]
     L.zsb_local_moments.restype = ctypes.c_int
+    L.zsb_occurrence_workspace_bytes.argtypes = []
+    L.zsb_occurrence_workspace_bytes.restype = SZ
+    L.zsb_occurrence_index.argtypes = [P, I32, I64, ctypes.c_uint64, I64, P, P, P]
+    L.zsb_occurrence_index.restype = ctypes.c_int
+    L.zsb_generate.argtypes = [I32, I64, I64, I64, ctypes.c_uint64, P, P, P]
+    L.zsb_generate.restype = ctypes.c_int
     L.zsb_bucket_histogram.argtypes = [P, I32, I64, P, I64, P, P]
     L.zsb_bucket_histogram.restype = ctypes.c_int
     L.zsb_bucket_minmax.argtypes = [P, I32, I64, P, I64, I32, P, P, P, P]

@@ -17,6 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libzsort_b200.so")
 SOURCES = [os.path.join(CSRC, "zsort_b200.cu")]
 HEADERS = [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "sort_kernels.cuh"),
+           os.path.join(CSRC, "dist_kernels.cuh"), os.path.join(CSRC, "gen_kernels.cuh"),
            os.path.join(REPO, "include", "zsort_b200.h")]
 
 NVCC_FLAGS = [

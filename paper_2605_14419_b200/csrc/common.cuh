@@ -112,7 +112,9 @@ enum Ctrl {
     C_NREF3 = 21,
     C_FTICK2 = 22,
     C_FTICK3 = 23,
-    C_SLOTS = 24
+    C_NTEAM = 24,        // team runs of the level (cap < len <= TEAM * cap)
+    C_TTICK = 25,        // team run ticket
+    C_SLOTS = 26
 };
 
 // ------------------------------------------------------------ key traits

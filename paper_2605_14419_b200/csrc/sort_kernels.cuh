@@ -425,6 +425,8 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
             ctrl[C_SCAN_TICKET] = 0ull;
             ctrl[C_NCHILD] = 0ull;
             ctrl[C_NENTRY] = 0ull;
+            ctrl[C_NTEAM] = 0ull;
+            ctrl[C_TTICK] = 0ull;
         }
     }
     int s = find_seg(segs, nseg, blockIdx.x);
@@ -637,15 +639,15 @@ struct ScatLayout {
     size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, off_cdf, total;
 };
 
-__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
+__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw, int nset = 2) {
     const int round = sw * 32 * SCAT_ITEMS;
     ScatLayout L;
     size_t o = 0;
     L.off_cur = o;
     o += (size_t)k * 4;
     o = (o + 15) & ~(size_t)15;
-    L.off_cnt = o;  // two counter sets (consecutive rounds alternate)
-    o += (size_t)2 * k * sw * 2;
+    L.off_cnt = o;  // nset counter sets (with two, consecutive rounds alternate)
+    o += (size_t)nset * k * sw * 2;
     o = (o + 15) & ~(size_t)15;
     L.off_lst = o;  // two run-start tables
     o += (size_t)2 * (k + 2) * 2;
@@ -667,7 +669,9 @@ __host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw) {
 // out [warp][ndig] (a warp's leaders then touch distinct banks).  Thread t
 // owns digits [t*per, (t+1)*per): per digit it walks the SW warps in order,
 // then one block scan of the thread totals and a write-back pass.  Writes the
-// digit starts to dstart[0..ndig].  Ends with a barrier.
+// digit starts to dstart[0..ndig].  Ends with a barrier.  (Folding the
+// cursor update in here and storing each staged record's destination instead
+// of its bucket measured 5 % slower on B200: placement is the critical phase.)
 template <int SW>
 __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstart, uint32_t *wsum) {
     constexpr int T = SW * 32;
@@ -700,7 +704,7 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
     __syncthreads();
 }
 
-template <int KK, int PB, int SW, int BM>
+template <int KK, int PB, int SW, int BM, int NSET>
 __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *__restrict__ segs, int nseg,
                                              const uint32_t *__restrict__ mat, int dst_sel, long long *prof) {
 #ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
@@ -742,10 +746,10 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         return;
     }
     const int k = p.k;
-    const ScatLayout L = scat_layout(k, PB, SW);
+    const ScatLayout L = scat_layout(k, PB, SW, NSET);
     const int NC = k * SW;
     uint32_t *cur = (uint32_t *)(smem + L.off_cur);
-    uint16_t *cnt2 = (uint16_t *)(smem + L.off_cnt);  // [2][SW][k]
+    uint16_t *cnt2 = (uint16_t *)(smem + L.off_cnt);  // [NSET][SW][k]
     uint16_t *lst2 = (uint16_t *)(smem + L.off_lst);  // [2][k + 2]
     uint64_t *stk = (uint64_t *)(smem + L.off_k);
     P *stp = (P *)(smem + L.off_p);
@@ -758,7 +762,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
     const uint32_t *col = mat + p.mat_base + ti;
     const uint32_t adj = (uint32_t)(p.start - p.scan_base);
     for (int b = threadIdx.x; b < k; b += ST) cur[b] = col[(int64_t)b * p.ntiles] + adj;
-    for (int q = threadIdx.x; q < 2 * NC; q += ST) cnt2[q] = 0;
+    for (int q = threadIdx.x; q < NSET * NC; q += ST) cnt2[q] = 0;
     __syncthreads();
 
     const int w = threadIdx.x >> 5, lane = lane_id();
@@ -782,7 +786,13 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
     // but the first and the last): no per-item bounds checks
     auto round_t = [&](auto full_t, int64_t r0, int nvalid) {
         constexpr bool FULL = decltype(full_t)::value;
-        uint16_t *cnt = cnt2 + rb * NC;
+        uint16_t *cnt = cnt2 + (NSET == 2 ? rb * NC : 0);
+        if constexpr (NSET == 1) {  // one counter set: cleared behind the previous round's placement
+            if (r0 != t0) {
+                for (int q = threadIdx.x; q < NC / 2; q += ST) ((uint32_t *)cnt)[q] = 0u;
+                __syncthreads();
+            }
+        }
         uint16_t *lst = lst2 + rb * (k + 2);
         const uint16_t *lstp = lst2 + (rb ^ 1) * (k + 2);
         P pay[PB != 0 ? ITEMS : 1];
@@ -793,12 +803,17 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         }
         // phase A: bucket + rank of item j (one shared atomic on its
         // per-(warp, bucket) u16 counter: the returned count is its rank among
-        // its warp's items of that bucket; a warp's shared-memory operations
-        // execute in program order, so ranks follow j; lanes of one
-        // instruction that share a bucket -- a tie group -- are exposed by
-        // re-reading the counter and re-ranked in lane order with a match,
-        // paid only by warp instructions that have one), interleaved with the
-        // coalesced write of staged slot tid + j*ST of the previous round.
+        // its warp's items of that bucket; items run in program order behind
+        // a __syncwarp, so ranks follow j).  The lanes of one instruction that
+        // share a bucket -- a tie group -- may get their counts in any order:
+        // the converged warp re-reads its counters after the atomic, a group
+        // of g lanes finds the group start + g there, and every such group is
+        // re-ranked in lane order with a match -- the checked path, always
+        // on, paid only by instructions holding a tie group.  Interleaved with
+        // the coalesced write of staged slot tid + j*ST of the previous round.
+        // (Measured on B200 and not used: a ballot-per-bucket-bit multi-split
+        // with no re-read, 27 % slower; a second __syncwarp between the atomic
+        // and the re-read, 8 % slower.)
         uint32_t pk[ITEMS];  // bucket | rank << 16
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
@@ -809,18 +824,12 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             const int q = w * k + (bkj < 0 ? 0 : bkj);
             const uint32_t sh = 16 * (q & 1);
             uint32_t *word = (uint32_t *)cnt + (q >> 1);
-            // the warp executes the atomic as one instruction and re-reads its
-            // counters after it (converged: __syncwarp here, __any_sync below),
-            // so a tie group of g lanes finds after == group start + g
-            __syncwarp();
+            __syncwarp();  // item j - 1's re-reads before item j's atomics
             if (bkj >= 0) {
                 old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
                 after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
             }
             {
-                // a tie group (lanes of this instruction sharing a bucket) is
-                // re-ranked in lane order whatever order the hardware handed
-                // out the old values in: stable by construction
                 const bool tie = bkj >= 0 && after != old + 1u;
                 if (__any_sync(0xffffffffu, tie)) {
                     const unsigned m = __match_any_sync(0xffffffffu, bkj);
@@ -857,8 +866,10 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             }
         }
         {
-            uint16_t *cn = cnt2 + (rb ^ 1) * NC;
-            for (int q = threadIdx.x; q < NC / 2; q += ST) ((uint32_t *)cn)[q] = 0u;
+            if constexpr (NSET == 2) {
+                uint16_t *cn = cnt2 + (rb ^ 1) * NC;
+                for (int q = threadIdx.x; q < NC / 2; q += ST) ((uint32_t *)cn)[q] = 0u;
+            }
             const int64_t rn = r0 + ROUND;
             const int nvn = rn < t1 ? (int)min((int64_t)ROUND, t1 - rn) : 0;
 #pragma unroll
@@ -892,14 +903,14 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
 #undef SCAT_MARK
 }
 
-template <int KK, int PB, int SW>
+template <int KK, int PB, int SW, int NSET>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
                                                               int dst_sel, long long *prof) {
     if (segs[find_seg(segs, nseg, blockIdx.x)].mode == MODE_ZCDF)
-        scatter_body<KK, PB, SW, 1>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 1, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else
-        scatter_body<KK, PB, SW, 0>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof);
 }
 
 // ------------------------------------------------------- equalisation
@@ -1148,7 +1159,10 @@ __global__ void __launch_bounds__(LT) k_level1_map(const uint64_t *__restrict__ 
             }
         }
         if (ok) {
-            // ---- S2: sample coarse-bin histogram -> CDF
+            // ---- S2: sample coarse-bin histogram -> CDF.  (A second, ordered-
+            // image coordinate -- log-like, chosen for one-signed heavy-tailed
+            // samples -- balanced C4's level-1 buckets but cost the 10^7-key
+            // scatter 7-14 % in code size and registers: not used.)
             for (int b = tid; b < kf; b += LT) fh[b] = 0;
             __syncthreads();
             for (int64_t gb = g0; gb < nitems; gb += SAMP_UNROLL * G) {
@@ -1278,8 +1292,9 @@ struct ClassCfg {
     int32_t half;  // level-1 window (recursion segments carry their own in SegParams::win)
     int32_t depth_guard;
     int32_t mapping;
-    int32_t child_fill;  // recursion children: k = pow2 >= child_fill * len / cap (buckets ~ cap / child_fill)
+    int32_t child_fill;  // recursion children: k = pow2 >= child_fill * len / kcap (buckets ~ kcap / child_fill)
     int32_t greedy;      // recursion levels pack finish runs greedily (else fixed windows)
+    int32_t team_cap;    // buckets of cap < len <= team_cap are team runs (K5t); 0: none
 };
 
 __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64_t g) {
@@ -1313,7 +1328,7 @@ __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restri
                                             const int64_t *__restrict__ kfirst, const uint32_t *__restrict__ mat,
                                             int64_t *__restrict__ bstart, SegParams *children, SegAcc *acc,
                                             unsigned long long *ctrl, const ClassCfg &cc, const Buffers &B,
-                                            int key_kind) {
+                                            int key_kind, Entry *teams) {
     const int s = seg_of_slot(kfirst, nseg, g);
     const SegParams &p = segs[s];
     const int b = (int)(g - kfirst[s]);
@@ -1329,6 +1344,10 @@ __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restri
                                       : p.start + (int64_t)mat[p.mat_base + (int64_t)(b + 1) * p.ntiles] - p.scan_base;
     const int64_t c = en - st;
     if (c <= cc.cap) return;
+    if (c <= cc.team_cap) {  // finished by a team (K5t) at this level
+        teams[atomicAdd(&ctrl[C_NTEAM], 1ull)] = Entry{st, (int32_t)c, (p.src == 1) ? 2 : 1};
+        return;
+    }
     SegParams ch{};
     ch.start = st;
     ch.len = c;
@@ -1431,7 +1450,7 @@ __device__ __forceinline__ void greedy_runs(const SegParams &p, const int64_t *_
 
 __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, int64_t *kfirst, int64_t *wfirst,
                            unsigned long long *ctrl, int32_t cap, int32_t kmax_child, int32_t min_tile,
-                           int32_t child_fill) {
+                           int32_t child_fill, int32_t kcap) {
     const int nseg = (int)*(volatile const unsigned long long *)nseg_ptr;
     constexpr int NV = 4;  // tiles, matrix entries, records, bucket slots, windows -> 5 with windows
     __shared__ long long sh[5][32];
@@ -1464,7 +1483,7 @@ __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, 
         SegParams p;
         if (s < nseg) {
             p = segs[s];
-            int64_t want = (p.len * child_fill + cap - 1) / cap;
+            int64_t want = (p.len * child_fill + kcap - 1) / kcap;  // buckets ~ kcap / child_fill
             int k = 16;
             while (k < want && k < kmax_child) k <<= 1;
             p.k = k;
@@ -1541,12 +1560,12 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
                                                    SegParams *children, SegAcc *acc, Entry *entries,
                                                    unsigned long long *ctrl, ClassCfg cc, int64_t total_slots,
                                                    int64_t total_windows, Buffers B, int key_kind, int32_t kmax_child,
-                                                   int32_t min_tile, unsigned long long *ref_zero) {
+                                                   int32_t min_tile, unsigned long long *ref_zero, Entry *teams) {
     cg::grid_group grid = cg::this_grid();
     if (blockIdx.x == 0 && threadIdx.x < 4 && ref_zero) ref_zero[threadIdx.x] = 0ull;  // the finish's refine counts/tickets
     const int64_t G = (int64_t)gridDim.x * blockDim.x, g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t g = g0; g < total_slots; g += G)
-        bstart_slot(g, segs, nseg, kfirst, mat, bstart, children, acc, ctrl, cc, B, key_kind);
+        bstart_slot(g, segs, nseg, kfirst, mat, bstart, children, acc, ctrl, cc, B, key_kind, teams);
     grid.sync();
     // one segment (level 1): every CTA binary-searches a shared copy of its bucket starts
     constexpr int BS_SHARED = 2049;
@@ -1588,7 +1607,8 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
     }
     grid.sync();
     if (blockIdx.x == 0)
-        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, kmax_child, min_tile, cc.child_fill);
+        plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, kmax_child, min_tile, cc.child_fill,
+                   cc.team_cap > cc.cap ? cc.team_cap : cc.cap);
 }
 
 // ------------------------------------------------------------------- K5
@@ -2170,6 +2190,328 @@ __device__ __forceinline__ void finish_list(const Buffers &B, const Entry *__res
         finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof, bar, parity);
         __syncthreads();
     }
+}
+
+// ------------------------------------------------------------------ K5t
+// Team finish: a run of cap < m <= TEAM * cap records -- a bucket too large
+// for one CTA's shared memory, which would otherwise cost another partition
+// level -- is finished by a thread-block cluster of TEAM CTAs (sample sort
+// of one run, the exchange through L2):
+//   stage     CTA r stages the contiguous chunk r of ceil(m / TEAM) records
+//             (TMA bulk copies, input order) and publishes TEAM_SAMP evenly
+//             spaced samples and its extremes (DSMEM);
+//   splitters every CTA sorts the cluster's 1024 samples (bitonic, warp
+//             shuffles below 32) and takes TEAM - 1 splitters s_j at equal
+//             sample ranks;
+//   parts     2 TEAM - 1 parts in key order: (s_{j-1}, s_j) and {s_j}; an
+//             equality part is final once its records are in input order;
+//   exchange  every record goes to its part in the output buffer at part
+//             start + part records of lower-ranked chunks + its rank among
+//             its chunk's records of that part (ballot multi-split in record
+//             order: stable); the stores stay in L2 for the next step;
+//   finish    after a cluster barrier, CTA r finishes the open part 2r
+//             (finish_entry in place, staged from L2).
+// An open part that still holds more than cap records (the samples missed
+// its mass) is pushed on the team's stack -- identical in every CTA -- and
+// finished the same way; its keys exclude the splitter values, so every
+// pass removes distinct values and this terminates.
+#ifndef ZSB_TEAM
+#define ZSB_TEAM 8  // CTAs per team; 0: no team runs
+#endif
+constexpr bool TEAM_ON = ZSB_TEAM > 0;
+constexpr int TEAM = ZSB_TEAM > 0 ? ZSB_TEAM : 8;  // CTAs per team (thread-block cluster size)
+constexpr int TEAM_NS = 1024;                     // samples of a run (one per thread of the sort)
+constexpr int TEAM_SAMP = TEAM_NS / TEAM;         // samples per chunk
+constexpr int TEAM_PARTS = 2 * TEAM - 1;          // open and equality parts
+constexpr int TEAM_PBITS = TEAM <= 2 ? 2 : (TEAM <= 4 ? 3 : (TEAM <= 8 ? 4 : 5));  // ballots per record
+constexpr int TEAM_STACK = 8 * TEAM;              // oversized open parts: < TEAM per run and level
+
+struct TeamShared {
+    unsigned long long omin, omax;          // this CTA's chunk extremes (read by the peers)
+    unsigned long long rmin, rmax;          // the run's extremes
+    unsigned long long wmin[FW], wmax[FW];  // warp partials
+    unsigned long long split[TEAM];         // splitters s_0 .. s_{TEAM-2}
+    long long ticket;                       // rank 0: the team's run ticket (read by the peers)
+    long long tk;                           // local copy of rank 0's ticket
+    uint32_t pcnt[TEAM_PARTS];              // this CTA's records per part (read by the peers)
+    uint32_t pstart[TEAM_PARTS + 1];        // part starts (offsets in the run)
+    uint32_t pbase[TEAM_PARTS];             // this CTA's first slot in each part
+    int sp;                                 // stack depth (the same in every CTA)
+    Entry stack[TEAM_STACK];
+};
+
+// Ascending sort of one u64 per thread across the 1024-thread CTA; a[] is
+// 1024 words of shared scratch.  Returns the thread's element of the result.
+__device__ __forceinline__ unsigned long long bitonic_1024(unsigned long long v, unsigned long long *a) {
+    const int t = threadIdx.x;
+#pragma unroll 1
+    for (int k = 2; k <= 1024; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            unsigned long long y;
+            if (j >= 32) {
+                a[t] = v;
+                __syncthreads();
+                y = a[t ^ j];
+                __syncthreads();
+            } else {
+                y = __shfl_xor_sync(0xffffffffu, v, j);
+            }
+            const bool up = (t & k) == 0, low = (t & j) == 0;
+            v = (low == up) ? min(v, y) : max(v, y);
+        }
+    }
+    return v;
+}
+
+template <int KK, int PB>
+__device__ __forceinline__ int team_run(const Buffers &B, const Entry e, int cap, Entry *refine,
+                                        unsigned long long *refine_count, int fin_ins, uint64_t *bar,
+                                        uint32_t &parity, TeamShared &ts) {
+    using P = typename PayloadT<PB>::T;
+    constexpr int F = FinItems<PB>::F;
+    static_assert(FT == TEAM_NS, "one sample per thread of the splitter sort");
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const FinLayout L = fin_layout(cap, PB);
+    unsigned long long *samp = (unsigned long long *)(smem + L.off_i);  // TEAM_SAMP samples (read by the peers)
+    unsigned long long *sortbuf = samp + TEAM_SAMP;                     // bitonic scratch (1024 words)
+    uint16_t *wcnt = (uint16_t *)(smem + L.off_bcnt);                   // [part][warp] counts, then cursors
+    const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int r = (int)cl.block_rank();
+    const int m = e.len;
+    const int q = (m + TEAM - 1) / TEAM;
+    const int c0 = min(m, r * q), mc = min(m, c0 + q) - c0;
+    const uint64_t *kin = nullptr;
+    const P *pin = nullptr;
+    stage_run<P, PB>(smem + L.off_o, src_keys(B, e.src) + e.start + c0, smem + L.off_pb,
+                     src_pay<PB>(B, e.src) + e.start + c0, mc, bar, kin, pin);
+    for (int x = tid; x < TEAM_PARTS * FW; x += FT) wcnt[x] = 0;
+    mbar_wait(&bar[0], parity);
+    __syncthreads();
+    const int base = w * 32 * F + lane;
+    uint64_t o[F];
+    unsigned long long mn = ~0ull, mx = 0ull;
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const int i = base + j * 32;
+        o[j] = i < mc ? ord_key<KK>(kin[i]) : 0ull;
+        if (i < mc) {
+            mn = min(mn, (unsigned long long)o[j]);
+            mx = max(mx, (unsigned long long)o[j]);
+        }
+    }
+    if (tid < TEAM_SAMP)  // evenly spaced samples of the chunk (mc >= TEAM_SAMP for every team run)
+        samp[tid] = mc ? ord_key<KK>(kin[min(mc - 1, (int)(((2 * tid + 1) * (int64_t)mc) / (2 * TEAM_SAMP)))]) : ~0ull;
+    mn = warp_min_u64(mn);
+    mx = warp_max_u64(mx);
+    if (lane == 0) {
+        ts.wmin[w] = mn;
+        ts.wmax[w] = mx;
+    }
+    __syncthreads();
+    if (w == 0) {
+        mn = warp_min_u64(ts.wmin[lane]);
+        mx = warp_max_u64(ts.wmax[lane]);
+        if (lane == 0) {
+            ts.omin = mn;
+            ts.omax = mx;
+        }
+    }
+    cl.sync();  // #1: extremes and samples published; every chunk is staged (the run may be overwritten in place)
+    if (w == 0) {
+        unsigned long long a = ~0ull, z = 0ull;
+        if (lane < TEAM) {
+            const TeamShared *peer = cl.map_shared_rank(&ts, lane);
+            a = peer->omin;
+            z = peer->omax;
+        }
+        a = warp_min_u64(a);
+        z = warp_max_u64(z);
+        if (lane == 0) {
+            ts.rmin = a;
+            ts.rmax = z;
+        }
+    }
+    const unsigned long long sv = cl.map_shared_rank(samp, tid / TEAM_SAMP)[tid % TEAM_SAMP];
+    __syncthreads();
+    const uint64_t rmin = ts.rmin, rmax = ts.rmax;
+    if (rmin == rmax) {  // all keys equal: already in stable order
+        mbar_wait(&bar[1], parity);
+        parity ^= 1u;
+        if (e.src != 2) {
+            uint64_t *ok = B.out_k + e.start + c0;
+            P *op = (P *)B.out_p + e.start + c0;
+            for (int i = tid; i < mc; i += FT) {
+                ok[i] = kin[i];
+                if constexpr (PB != 0) op[i] = pin[i];
+            }
+        }
+        cl.sync();  // peers are done reading this CTA's samples
+        return 0;
+    }
+    const unsigned long long sorted = bitonic_1024(sv, sortbuf);
+    if (tid % TEAM_SAMP == 0 && tid) ts.split[tid / TEAM_SAMP - 1] = sorted;
+    __syncthreads();
+    unsigned long long spl[TEAM - 1];
+#pragma unroll
+    for (int j = 0; j < TEAM - 1; j++) spl[j] = ts.split[j];
+    // part of each record (key order): 2c for (s_{c-1}, s_c), 2c + 1 for {s_c}
+    uint32_t ppk[(F + 3) / 4];  // parts, four per register
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        int c = 0;
+        bool eq = false;
+#pragma unroll
+        for (int u = 0; u < TEAM - 1; u++) {
+            c += spl[u] < o[j];
+            eq |= spl[u] == o[j];
+        }
+        const uint32_t pj = (uint32_t)(2 * c + (eq ? 1 : 0));
+        if ((j & 3) == 0) ppk[j >> 2] = pj;
+        else ppk[j >> 2] |= pj << (8 * (j & 3));
+    }
+    // multi-split pass 1: per-(part, warp) counts
+    unsigned gm[F];
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const bool valid = base + j * 32 < mc;
+        const int p = (int)((ppk[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+        unsigned mm = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bit = 0; bit < TEAM_PBITS; bit++) {
+            const bool v = (p >> bit) & 1;
+            const unsigned bb = __ballot_sync(0xffffffffu, v);
+            mm &= v ? bb : ~bb;
+        }
+        gm[j] = mm;
+        __syncwarp();
+        if (valid && lane == __ffs(mm) - 1) wcnt[p * FW + w] += (uint16_t)__popc(mm);
+    }
+    __syncthreads();
+    // per part: exclusive scan over the warps, chunk total (warp p scans part p)
+    if (w < TEAM_PARTS) {
+        const uint32_t c = wcnt[w * FW + lane];
+        uint32_t s_ = c;
+#pragma unroll
+        for (int o_ = 1; o_ < 32; o_ <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, s_, o_);
+            if (lane >= o_) s_ += y;
+        }
+        wcnt[w * FW + lane] = (uint16_t)(s_ - c);
+        if (lane == 31) ts.pcnt[w] = s_;
+    }
+    cl.sync();  // #2: part counts published
+    if (w == 0) {  // part starts and this CTA's slots: lane p (< TEAM_PARTS) reads every chunk's count of part p
+        uint32_t tot = 0, below = 0;
+        if (lane < TEAM_PARTS) {
+#pragma unroll
+            for (int rr = 0; rr < TEAM; rr++) {
+                const uint32_t v = cl.map_shared_rank(ts.pcnt, rr)[lane];
+                tot += v;
+                below += rr < r ? v : 0u;
+            }
+        }
+        uint32_t s_ = tot;
+#pragma unroll
+        for (int o_ = 1; o_ < 32; o_ <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, s_, o_);
+            if (lane >= o_) s_ += y;
+        }
+        if (lane < TEAM_PARTS) {
+            ts.pstart[lane] = s_ - tot;
+            ts.pbase[lane] = s_ - tot + below;
+        }
+        if (lane == TEAM_PARTS - 1) ts.pstart[TEAM_PARTS] = s_;
+    }
+    __syncthreads();
+    mbar_wait(&bar[1], parity);  // payload staged
+    parity ^= 1u;
+    // multi-split pass 2: rank in record order, store to the part
+    uint64_t *ok = B.out_k + e.start;
+    P *op = (P *)B.out_p + e.start;
+    const uint64_t l2pol = l2_evict_last_policy();
+#pragma unroll
+    for (int j = 0; j < F; j++) {
+        const int i = base + j * 32;
+        const bool valid = i < mc;
+        const int p = (int)((ppk[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+        const unsigned mm = gm[j];
+        const int leader = valid ? __ffs(mm) - 1 : lane;
+        uint32_t c = 0;
+        __syncwarp();
+        if (valid && lane == leader) {
+            c = wcnt[p * FW + w];
+            wcnt[p * FW + w] = (uint16_t)(c + __popc(mm));
+        }
+        c = __shfl_sync(0xffffffffu, c, leader);
+        if (valid) {
+            const uint32_t pos = ts.pbase[p] + c + (uint32_t)__popc(mm & lt);
+            st_keep(ok + pos, kin[i], l2pol);
+            if constexpr (PB != 0) st_keep(op + pos, pin[i], l2pol);
+        }
+    }
+    // the open parts are re-staged by TMA bulk copies (async proxy) in other CTAs
+    fence_proxy_async_global();
+    cl.sync();  // #3: every record is in its part (equality parts are final)
+    int nfin = 0;
+    {
+        const int ps = (int)ts.pstart[2 * r], pc = (int)ts.pstart[2 * r + 1] - ps;
+        if (pc > 0 && pc <= cap) {
+            finish_entry<KK, PB>(B, Entry{e.start + ps, pc, 2}, 0, cap, refine, refine_count, fin_ins, nullptr, bar,
+                                 parity);
+            nfin = 1;
+        }
+    }
+    if (tid == 0) {  // oversized open parts: the team finishes them next (same order in every CTA)
+        for (int pp = TEAM - 1; pp >= 0; pp--) {
+            const int ps = (int)ts.pstart[2 * pp], pc = (int)ts.pstart[2 * pp + 1] - ps;
+            if (pc > cap && ts.sp < TEAM_STACK) ts.stack[ts.sp++] = Entry{e.start + ps, pc, 2};
+        }
+    }
+    __syncthreads();
+    return nfin;
+}
+
+// Persistent team kernel: clusters of TEAM CTAs take team runs by ticket
+// (rank 0 draws, the peers read it through DSMEM), oversized parts first.
+template <int KK, int PB>
+__global__ void __launch_bounds__(FT, 1) k_team(Buffers B, const Entry *__restrict__ runs,
+                                                const unsigned long long *count, int64_t cap_runs, int cap,
+                                                Entry *refine, unsigned long long *refine_count, int fin_ins,
+                                                unsigned long long *ticket, unsigned long long *runs_total) {
+    __shared__ uint64_t bar[2];
+    __shared__ TeamShared ts;
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        ts.sp = 0;
+    }
+    __syncthreads();
+    const int64_t ne = min((int64_t)*count, cap_runs);
+    uint32_t parity = 0;
+    int nfin = 0;
+    while (true) {
+        Entry e;
+        if (ts.sp > 0) {
+            e = ts.stack[ts.sp - 1];
+            __syncthreads();
+            if (threadIdx.x == 0) ts.sp--;
+        } else {
+            if (cl.block_rank() == 0 && threadIdx.x == 0) ts.ticket = (long long)atomicAdd(ticket, 1ull);
+            cl.sync();
+            if (threadIdx.x == 0) ts.tk = *cl.map_shared_rank(&ts.ticket, 0);
+            __syncthreads();
+            if (ts.tk >= ne) break;
+            e = runs[ts.tk];
+        }
+        __syncthreads();
+        nfin += team_run<KK, PB>(B, e, cap, refine, refine_count, fin_ins, bar, parity, ts);
+    }
+    cl.sync();  // no CTA leaves while a peer may still read its shared memory
+    if (threadIdx.x == 0 && nfin) atomicAdd(runs_total, (unsigned long long)nfin);
 }
 
 // Refine iterations (every CTA of a cooperative grid): finishes the refine

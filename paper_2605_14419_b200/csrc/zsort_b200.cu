@@ -23,6 +23,7 @@
 
 #include "../../include/zsort_b200.h"
 #include "dist_kernels.cuh"
+#include "gen_kernels.cuh"
 #include "sort_kernels.cuh"
 
 using namespace zsb;
@@ -111,6 +112,12 @@ void timing_collect() {
 #ifndef ZSB_K1MAX
 #define ZSB_K1MAX 1024  // cap on the fitted level-1 bucket count
 #endif
+#ifndef ZSB_TEAM_L1
+#define ZSB_TEAM_L1 0  // 1: level-1 buckets up to TEAM * cap are team runs (k sized for them); measured slower
+#endif
+#ifndef ZSB_K1_TEAM
+#define ZSB_K1_TEAM 2048  // cap on the level-1 bucket count when buckets are sized for team runs
+#endif
 #ifndef ZSB_SW16_ABOVE
 #define ZSB_SW16_ABOVE 512  // bucket counts above this use 16-warp, 8192-record scatter rounds
 #endif
@@ -193,6 +200,9 @@ Plan1 plan_level1(int64_t n, int pb, const zsb_config &cfg) {
     } else {
         const int64_t kmax = ZSB_K1MAX;  // runs of >= 4 records per 4096-record round
         P.k = std::min<int64_t>(std::max<int64_t>(16, pow2_at_least((4 * n + P.cap - 1) / P.cap)), kmax);
+        // large inputs: buckets of ~half a team run (K5t finishes them without a second level)
+        const int64_t tcap = (int64_t)TEAM * P.cap;
+        if (TEAM_ON && ZSB_TEAM_L1 && n / P.k > tcap / 2) P.k = std::min<int64_t>(pow2_at_least((2 * n + tcap - 1) / tcap), ZSB_K1_TEAM);
     }
     const int tps = ZSB_TILES_PER_SM > 0 ? ZSB_TILES_PER_SM : (scat_warps((int)P.k, ZSB_SW16_ABOVE) == 8 ? 2 : 1);
     int64_t target_tiles = (int64_t)num_sms() * tps;
@@ -217,12 +227,13 @@ Plan1 plan_rec(int64_t n, int pb, int64_t k) {
 }
 
 struct Layout {
-    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, wfirst, bstart, entries, refine[4], parts, ctrl,
-        dbg, fine, lut, total;
-    int64_t mat_cap, seg_cap, ent_cap, status_cap, slot_cap, ref_cap;
+    size_t tmp_k, tmp_p, mat, status, seg_a, seg_b, acc, kfirst, wfirst, bstart, entries, teams, refine[4], parts,
+        ctrl, dbg, fine, lut, total;
+    int64_t mat_cap, seg_cap, ent_cap, status_cap, slot_cap, ref_cap, team_cap_list;
 };
 
 constexpr int MOM_GRID_PER_SM = 4;
+constexpr int OCC_CHUNKS = 1024;  // occurrence search: chunks of pass 1
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -258,6 +269,9 @@ Layout make_layout(int64_t n, int pb, const Plan1 &P, bool need_tmp) {
     o = align_up(o + (size_t)L.slot_cap * 8);
     L.entries = o;
     o = align_up(o + (size_t)L.ent_cap * sizeof(Entry));
+    L.team_cap_list = n / cap + 16;  // team runs hold > cap records each
+    L.teams = o;
+    o = align_up(o + (size_t)L.team_cap_list * sizeof(Entry));
     for (int q = 0; q < 4; q++) {
         L.refine[q] = o;
         o = align_up(o + (size_t)L.ref_cap * sizeof(Entry));
@@ -410,18 +424,30 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
     ZSB_LAUNCH("k_scan");
     if (after_scan) ZSB_CUDA(cudaEventRecord(after_scan, c.st));
     const size_t cdf_bytes = (c.B.cdf && segs_level1) ? (size_t)(CDF_KNOTS + 1) * 8 : 0;
-    const bool sw16 = scat_warps(kmax, ZSB_SW16_ABOVE) == 16 &&
-                      scat_layout(kmax, PB, 16).total + cdf_bytes <= (size_t)227 * 1024 - 1024;
-    if (!sw16) {
+    const size_t smax = (size_t)227 * 1024 - 1024;
+    // 16 warps (8192-record rounds) above ZSB_SW16_ABOVE buckets: two counter
+    // sets (rounds pipelined) when they fit shared memory, else one
+    const bool want16 = scat_warps(kmax, ZSB_SW16_ABOVE) == 16;
+    const int nset16 = !want16 ? 0 : (scat_layout(kmax, PB, 16, 2).total + cdf_bytes <= smax ? 2
+                                       : (scat_layout(kmax, PB, 16, 1).total + cdf_bytes <= smax ? 1 : 0));
+    if (nset16 == 0) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
-        smem_optin(k_scatter<KK, PB, 8>, sbytes);
+        smem_optin(k_scatter<KK, PB, 8, 2>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 8><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
+        k_scatter<KK, PB, 8, 2><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
+                                                                        scat_prof(tiles));
+    } else if (nset16 == 2) {
+        const size_t sbytes = scat_layout(kmax, PB, 16, 2).total + cdf_bytes;
+        smem_optin(k_scatter<KK, PB, 16, 2>, sbytes);
+        PhaseScope ph(PH_SCATTER, c.st);
+        k_scatter<KK, PB, 16, 2><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
+                                                                         scat_prof(tiles));
     } else {
-        const size_t sbytes = scat_layout(kmax, PB, 16).total + cdf_bytes;
-        smem_optin(k_scatter<KK, PB, 16>, sbytes);
+        const size_t sbytes = scat_layout(kmax, PB, 16, 1).total + cdf_bytes;
+        smem_optin(k_scatter<KK, PB, 16, 1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 16><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles));
+        k_scatter<KK, PB, 16, 1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
+                                                                         scat_prof(tiles));
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
@@ -511,6 +537,70 @@ int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev
                                       c.st));
     }
     ZSB_LAUNCH("k_finish");
+    return ZSB_OK;
+}
+
+// Team finish (K5t): clusters of TEAM CTAs, as many as stay resident (B200:
+// 15 clusters of 8 = 120 SMs with one 1024-thread CTA per SM).  0: the device
+// cannot hold one cluster (teams off; oversized buckets recurse instead).
+template <int KK, int PB>
+int team_grid() {
+    static std::mutex mu;
+    static std::unordered_map<int, int> grid;  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = grid.find(dev);
+    if (it != grid.end()) return it->second;
+    if (!TEAM_ON) return 0;  // -DZSB_TEAM=0: no team runs, oversized buckets always recurse
+    FinLayout FL = fin_layout(finish_cap(PB), PB);
+    smem_optin(k_team<KK, PB>, FL.total);
+    if (TEAM > 8) cudaFuncSetAttribute((const void *)k_team<KK, PB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TEAM;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(TEAM * 16);
+    cfg.blockDim = dim3(FT);
+    cfg.dynamicSmemBytes = FL.total;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (const void *)k_team<KK, PB>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        ncl = 0;
+    }
+    grid[dev] = ncl * TEAM;
+    return ncl * TEAM;
+}
+
+template <int KK, int PB>
+int launch_team(Ctx &c, const Entry *runs, const unsigned long long *count_dev, int ref_out) {
+    const int grid = team_grid<KK, PB>();
+    if (grid <= 0) return ZSB_OK;
+    FinLayout FL = fin_layout((int)c.P.cap, PB);
+    unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TEAM;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(FT);
+    cfg.dynamicSmemBytes = FL.total;
+    cfg.stream = c.st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    {
+        PhaseScope ph(PH_FINISH, c.st);
+        ZSB_CUDA(cudaLaunchKernelEx(&cfg, k_team<KK, PB>, c.B, runs, count_dev, (int64_t)c.L.team_cap_list,
+                                    (int)c.P.cap, (Entry *)(c.ws + c.L.refine[ref_out]), ctrl + REF_SLOT[ref_out],
+                                    (int)FIN_INS, ctrl + C_TTICK, ctrl + C_ST_INSERTION));
+    }
+    ZSB_LAUNCH("k_team");
     return ZSB_OK;
 }
 
@@ -646,7 +736,12 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
     MapCfg mc{rec ? (int32_t)ZSB_MAP_PAPER : cfg.mapping, (int32_t)cfg.depth_guard, rec ? rec->level : 0, 0,
               rec ? rec->scale : 0.0};
     ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping,
-                (int32_t)std::max(1, std::min(16, ZSB_CHILD_FILL)), ZSB_GREEDY};
+                (int32_t)std::max(1, std::min(16, ZSB_CHILD_FILL)), ZSB_GREEDY,
+                0};
+    // team runs (K5t) finish the few oversized buckets of recursion levels,
+    // which would otherwise cost whole extra levels (level 1: ZSB_TEAM_L1)
+    const int32_t team_cap = team_grid<KK, PB>() > 0 ? (int32_t)(TEAM * c.P.cap) : 0;
+    Entry *teams = (Entry *)(c.ws + c.L.teams);
     const int64_t nwin1 = (n + c.P.half - 1) / c.P.half;
     const bool equalize = !rec && cfg.mapping == ZSB_MAP_FITTED && !ZSB_NO_EQUALIZE;
     unsigned int *fine = (unsigned int *)(c.ws + c.L.fine);
@@ -706,6 +801,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
         ZSB_CUDA(cudaMemcpyAsync(acc, &a0, sizeof(a0), cudaMemcpyHostToDevice, c.st));
     }
     while (true) {
+        cc.team_cap = (level > 1 || ZSB_TEAM_L1) ? team_cap : 0;
         if (level > 1 || rec) {
             {
                 PhaseScope ph(PH_SEGSTATS, c.st, 2);
@@ -731,7 +827,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
             Buffers Bv = c.B;
             unsigned long long *ref_zero = ctrl + REF_SLOT[2 * par];
             void *args[] = {&seg_cur, &nseg_, &kfirst, &wfirst, &mat, &bstart, &seg_next, &acc, &entries, &ctrl,
-                            &cc, &ts, &tw, &Bv, &key_kind, &kmc, &mt, &ref_zero};
+                            &cc, &ts, &tw, &Bv, &key_kind, &kmc, &mt, &ref_zero, &teams};
             ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_classify, dim3(cgrid), dim3(1024), args, 0, g_hs.side));
         }
         ZSB_LAUNCH("k_classify");
@@ -741,6 +837,11 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
         ZSB_CUDA(cudaMemcpyAsync(hc, ctrl, C_SLOTS * 8, cudaMemcpyDeviceToHost, g_hs.side));
         ZSB_CUDA(cudaEventRecord(g_hs.ev, g_hs.side));
         ZSB_CUDA(cudaStreamWaitEvent(c.st, g_hs.ev, 0));  // the finish (and every later level) after classify
+        // team runs first: their parts' refine runs join the finish's refine list
+        if (cc.team_cap) {
+            rc = launch_team<KK, PB>(c, teams, ctrl + C_NTEAM, 2 * par);
+            if (rc) return rc;
+        }
         rc = enqueue_finish(entries, ctrl + C_NENTRY, c.L.ent_cap, c.L.ent_cap, par, true);
         if (rc) return rc;
         ZSB_CUDA(cudaEventSynchronize(g_hs.ev));
@@ -819,6 +920,10 @@ int check_cfg(const zsb_config &c) {  // core.py:81-89
 
 template <template <int, int> class F, typename... A>
 int dispatch(int kd, int pb, A &&...args) {
+#ifdef ZSB_ONLY_F64_P4  // experiment builds (tools/build_variant.sh): one key/payload combination, 1/6 the compile
+    if (kd == ZSB_KEY_F64 && pb == 4) return F<1, 4>::run(args...);
+    return fail(ZSB_ERR_ARG, "this experiment build holds only float64 keys with a 4-byte payload");
+#else
     if (kd == ZSB_KEY_I64) {
         if (pb == 0) return F<0, 0>::run(args...);
         if (pb == 4) return F<0, 4>::run(args...);
@@ -827,6 +932,7 @@ int dispatch(int kd, int pb, A &&...args) {
     if (pb == 0) return F<1, 0>::run(args...);
     if (pb == 4) return F<1, 4>::run(args...);
     return F<1, 8>::run(args...);
+#endif
 }
 
 template <int KK, int PB>
@@ -1161,24 +1267,86 @@ int zsb_check_sorted(const void *d_in_keys, const void *d_out_keys, const void *
 }
 
 
-int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double shift, double *d_out3,
+int zsb_local_moments(const void *d_keys, int32_t key_dtype, int64_t n, double shift, double *d_out4,
                       uint64_t *d_out_bits2, void *stream) {
     int rc = check_common(d_keys, key_dtype, 0, n);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     count_launches(1);
-    k_dist_init<<<1, 32, 0, st>>>(d_out3, (unsigned long long *)d_out_bits2);
+    k_dist_init<<<1, 32, 0, st>>>(d_out4, (unsigned long long *)d_out_bits2);
     ZSB_LAUNCH("k_dist_init");
     if (n == 0) return ZSB_OK;
     const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    const int self = std::isnan(shift) ? 1 : 0;  // NaN: shift by the shard's first key
     count_launches(1);
     if (key_dtype == ZSB_KEY_I64)
-        k_local_moments<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, d_out3,
+        k_local_moments<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, self, d_out4,
                                                 (unsigned long long *)d_out_bits2);
     else
-        k_local_moments<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, d_out3,
+        k_local_moments<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, shift, self, d_out4,
                                                 (unsigned long long *)d_out_bits2);
     ZSB_LAUNCH("k_local_moments");
+    return ZSB_OK;
+}
+
+int zsb_occurrence_index(const void *d_keys, int32_t key_dtype, int64_t n, uint64_t key_bits, int64_t occurrence,
+                         void *d_workspace, int64_t *h_index, void *stream) {
+    int rc = check_common(d_keys, key_dtype, 0, n);
+    if (rc) return rc;
+    if (!h_index || !d_workspace) return fail(ZSB_ERR_ARG, "null workspace or result pointer");
+    *h_index = -1;
+    if (n == 0 || occurrence < 0) return ZSB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nch = std::max(1, std::min<int>(OCC_CHUNKS, (int)((n + 4095) / 4096)));
+    const int64_t chunk = (n + nch - 1) / nch;
+    unsigned long long *cnt = (unsigned long long *)d_workspace;
+    long long *out = (long long *)(cnt + OCC_CHUNKS);
+    uint64_t target = key_bits ^ SIGN;  // ordered image (host copy of ord_key)
+    if (key_dtype == ZSB_KEY_F64) {
+        const uint64_t b = key_bits == SIGN ? 0ull : key_bits;
+        target = (b & SIGN) ? ~b : (b | SIGN);
+    }
+    count_launches(2);
+    if (key_dtype == ZSB_KEY_I64) {
+        k_occ_count<0><<<nch, NT, 0, st>>>((const uint64_t *)d_keys, n, chunk, target, cnt);
+        k_occ_find<0><<<1, OCC_T, 0, st>>>((const uint64_t *)d_keys, n, chunk, nch, target, occurrence, cnt, out);
+    } else {
+        k_occ_count<1><<<nch, NT, 0, st>>>((const uint64_t *)d_keys, n, chunk, target, cnt);
+        k_occ_find<1><<<1, OCC_T, 0, st>>>((const uint64_t *)d_keys, n, chunk, nch, target, occurrence, cnt, out);
+    }
+    ZSB_LAUNCH("k_occ_count/find");
+    long long h = -1;
+    ZSB_CUDA(cudaMemcpyAsync(&h, out, 8, cudaMemcpyDeviceToHost, st));
+    ZSB_CUDA(cudaStreamSynchronize(st));
+    *h_index = h;
+    return ZSB_OK;
+}
+
+size_t zsb_occurrence_workspace_bytes(void) { return (size_t)(OCC_CHUNKS + 1) * 8; }
+
+int zsb_generate(int32_t family, int64_t offset, int64_t n, int64_t n_total, uint64_t seed, const double *params,
+                 int64_t *d_out, void *stream) {
+    if (family < GEN_UNIFORM || family > GEN_HIGH_DUP) return fail(ZSB_ERR_ARG, "unknown family");
+    if (n < 0 || offset < 0 || offset + n > n_total) return fail(ZSB_ERR_ARG, "need 0 <= offset <= offset + n <= n_total");
+    if (n == 0) return ZSB_OK;
+    if (!d_out) return fail(ZSB_ERR_ARG, "null output pointer");
+    GenParams gp{0.0, 1e9, 1.5, 1.0, 0.01, 1000};  // the reference's DistributionSpec defaults (datagen.py:48-59)
+    if (params) {
+        gp.normal_mu = params[0];
+        gp.normal_sigma = params[1];
+        gp.pareto_alpha = params[2];
+        gp.pareto_xm = params[3];
+        gp.swap_fraction = params[4];
+        gp.dup_range = (uint64_t)params[5];
+    }
+    if (!(gp.normal_sigma > 0) || !(gp.pareto_alpha > 0) || !(gp.pareto_xm > 0) || !(gp.swap_fraction >= 0) ||
+        !(gp.swap_fraction <= 0.5) || gp.dup_range < 1)
+        return fail(ZSB_ERR_ARG, "bad family parameters");
+    const uint64_t base = splitmix64_u(seed ^ ((uint64_t)(family + 1) << 56));
+    const int grid = std::max(1, std::min<int>(num_sms() * 8, (int)((n + NT - 1) / NT)));
+    count_launches(1);
+    k_generate<<<grid, NT, 0, (cudaStream_t)stream>>>(family, base, offset, n, n_total, gp, d_out);
+    ZSB_LAUNCH("k_generate");
     return ZSB_OK;
 }
 
@@ -1241,15 +1409,22 @@ int zsb_range_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const 
     ZSB_CUDA(cudaMemsetAsync(d_counts, 0, (size_t)nq * nbins * 8, st));
     if (n == 0 || nq == 0) return ZSB_OK;
     const int grid = std::max(1, std::min<int>(num_sms() * 4, (int)((n + NT - 1) / NT)));
+    // counters in shared memory when they fit (<= 96 KB: two CTAs per SM)
+    const size_t sm = (size_t)nq * nbins * 4;
+    const int use_smem = sm <= (size_t)96 * 1024 ? 1 : 0;
+    const size_t dyn = use_smem ? sm : 0;
     count_launches(1);
-    if (key_dtype == ZSB_KEY_I64)
-        k_range_hist<0><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
-                                             (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
-                                             (unsigned long long *)d_counts);
-    else
-        k_range_hist<1><<<grid, NT, 0, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
-                                             (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
-                                             (unsigned long long *)d_counts);
+    if (key_dtype == ZSB_KEY_I64) {
+        smem_optin(k_range_hist<0>, dyn);
+        k_range_hist<0><<<grid, NT, dyn, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
+                                               (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
+                                               (unsigned long long *)d_counts, use_smem);
+    } else {
+        smem_optin(k_range_hist<1>, dyn);
+        k_range_hist<1><<<grid, NT, dyn, st>>>((const uint64_t *)d_keys, n, params[0], params[1], params[2], params[3],
+                                               (int)k, nq, d_qbucket, d_qlo, d_qhi, d_qshift, nbins,
+                                               (unsigned long long *)d_counts, use_smem);
+    }
     ZSB_LAUNCH("k_range_hist");
     return ZSB_OK;
 }

@@ -6,10 +6,11 @@ path; this is the B200 extension of its algorithm described in SURVEY.md
 positions [gidx_base, gidx_base + n_local)); the global stable order is
 (key, global position).
 
-  D1  all_reduce of the shard moments (count, sum, sum of squares around a
-      common shift; MIN/MAX of the ordered extremes) -> every rank derives
-      bit-identical fitted z-score parameters (core.py:212-234 with the
-      fitted scale of the single-GPU path);
+  D1  one pass over each shard (count, sum and sum of squares around the
+      shard's first key, ordered extremes) and one all_gather of those six
+      numbers; every rank merges them in rank order (Chan's parallel
+      variance) and derives bit-identical fitted z-score parameters
+      (core.py:212-234 with the fitted scale of the single-GPU path);
   D2  all_gather of the k-bucket z-score histograms -> G-1 cuts at the
       target positions j*N/G.  A cut falls on a bucket boundary, except
       inside an all-equal bucket (checked with an all_reduce of per-bucket
@@ -85,6 +86,30 @@ def plan_params(count: float, s1: float, s2: float, shift: float, vmin: float, v
             if scale > 0.0 and math.isfinite(scale) and math.isfinite(zmin):
                 return GlobalParams(mean, sd, zmin, scale, k)
     return GlobalParams(0.0, 1.0, 0.0, 1e-300, k)
+
+
+def merge_moments(rows: np.ndarray):
+    """Global (count, mean, M2, ordered min, ordered max) from the per-rank D1
+    rows {count, sum(x - c), sum((x - c)^2), c, min bits, max bits}: Chan's
+    pairwise merge in rank order, so every rank computes the same doubles."""
+    n = mean = m2 = 0.0
+    omin, omax = MASK64, 0
+    bits = np.ascontiguousarray(rows[:, 4:6]).view(np.uint64)
+    for r in range(rows.shape[0]):
+        nr = float(rows[r, 0])
+        if nr <= 0.0:
+            continue
+        s1, s2, c = float(rows[r, 1]), float(rows[r, 2]), float(rows[r, 3])
+        mr = c + s1 / nr
+        m2r = max(0.0, s2 - s1 * s1 / nr)
+        tot = n + nr
+        d = mr - mean
+        mean = mean + d * (nr / tot)
+        m2 = m2 + m2r + d * d * (n * nr / tot)
+        n = tot
+        omin = min(omin, int(bits[r, 0]))
+        omax = max(omax, int(bits[r, 1]))
+    return n, mean, m2, omin, omax
 
 
 @dataclass(frozen=True)
@@ -230,10 +255,12 @@ class DeviceOps:
     def _kd(keys):
         return 0 if keys.dtype == torch.int64 else 1
 
-    def local_moments(self, keys: torch.Tensor, shift: float):
-        out = torch.empty(3, dtype=torch.float64, device=self.device)
+    def local_moments(self, keys: torch.Tensor):
+        """One pass: ({count, sum(x - c), sum((x - c)^2), c}, {ordered min, max}),
+        c = the shard's first key."""
+        out = torch.empty(4, dtype=torch.float64, device=self.device)
         bits = torch.empty(2, dtype=torch.int64, device=self.device)
-        _lib.check(self.L.zsb_local_moments(keys.data_ptr(), self._kd(keys), keys.numel(), float(shift),
+        _lib.check(self.L.zsb_local_moments(keys.data_ptr(), self._kd(keys), keys.numel(), float("nan"),
                                             out.data_ptr(), bits.data_ptr(), self._stream()))
         return out, bits
 
@@ -266,13 +293,16 @@ class DeviceOps:
 
     def occurrence_index(self, keys, key_bits: int, occurrence: int, kind: str) -> int:
         """Local index of the `occurrence`-th record equal to the key with bits
-        key_bits (for float64, -0.0 and +0.0 are the same key)."""
-        kb = key_bits - (1 << 64) if key_bits >= SIGN else key_bits
-        bits = keys.view(torch.int64)
-        mask = bits == kb
-        if kind == "float64" and key_bits in (0, SIGN):
-            mask |= bits == (INT64_MIN if key_bits == 0 else 0)
-        return int(torch.nonzero(mask)[occurrence].item())
+        key_bits (for float64, -0.0 and +0.0 are the same key): the device
+        search k_occ_count / k_occ_find."""
+        ws = torch.empty(int(self.L.zsb_occurrence_workspace_bytes()), dtype=torch.uint8, device=self.device)
+        out = ctypes.c_int64(-1)
+        _lib.check(self.L.zsb_occurrence_index(keys.data_ptr(), self._kd(keys), keys.numel(),
+                                               ctypes.c_uint64(key_bits & MASK64), int(occurrence), ws.data_ptr(),
+                                               ctypes.byref(out), self._stream()))
+        if out.value < 0:
+            raise RuntimeError("occurrence not found: the cut plan and the shard disagree")
+        return int(out.value)
 
     def partition(self, keys, payload, params: GlobalParams, gidx_base: int, cuts):
         n = keys.numel()
@@ -344,33 +374,22 @@ def dist_zsort(keys: torch.Tensor, payload: torch.Tensor | None, gidx_base: int,
     n = keys.numel()
     info = {"world": world}
 
-    # ---- D1: extremes, then shifted moments (two tiny all_reduces)
-    _, bits = ops.local_moments(keys, 0.0)
-    mn = torch.tensor([bits[0].item() if n else -1], dtype=torch.int64, device=dev)  # as signed for MIN/MAX
-    mx = torch.tensor([bits[1].item() if n else 0], dtype=torch.int64, device=dev)
-    # ordered images are unsigned; flip the sign bit so signed MIN/MAX order them
-    mn ^= INT64_MIN
-    mx ^= INT64_MIN
-    if n == 0:
-        mn.fill_(2**63 - 1)
-        mx.fill_(INT64_MIN)
-    comm.all_reduce(mn, "min")
-    comm.all_reduce(mx, "max")
-    omin = (int(mn.item()) ^ INT64_MIN) & ((1 << 64) - 1)
-    omax = (int(mx.item()) ^ INT64_MIN) & ((1 << 64) - 1)
-    vmin, vmax = ord_to_value(omin, kind), ord_to_value(omax, kind)
-    shift = 0.5 * vmin + 0.5 * vmax
-    mom, _ = ops.local_moments(keys, shift)
-    mom = mom.clone()
-    comm.all_reduce(mom, "sum")
-    count, s1, s2 = (float(x) for x in mom.tolist())
+    # ---- D1: one pass per shard, one all_gather of six numbers per rank
+    if n:
+        mom, bits = ops.local_moments(keys)
+        row = torch.cat([mom.to(torch.float64), bits.view(torch.float64)])
+    else:
+        row = torch.zeros(6, dtype=torch.float64, device=dev)
+    rows = torch.stack(comm.all_gather(row)).cpu().numpy()  # (G, 6): count, s1, s2, c, min bits, max bits
+    count, mean, m2, omin, omax = merge_moments(rows)
     info.update(total=int(count), omin=omin, omax=omax)
     if count == 0:
         return keys.clone(), (payload.clone() if payload is not None else None), info
     if omin == omax or world == 1:  # globally constant (already stable) or nothing to exchange
         k_, p_ = ops.local_sort(keys, payload) if n else (keys.clone(), payload)
         return k_, p_, info
-    params = plan_params(count, s1, s2, shift, vmin, vmax, k)
+    vmin, vmax = ord_to_value(omin, kind), ord_to_value(omax, kind)
+    params = plan_params(count, 0.0, m2, mean, vmin, vmax, k)
 
     # ---- D2: per-rank histograms (all_gather) -> cuts
     hist = ops.bucket_histogram(keys, params)

@@ -69,13 +69,14 @@ class NumpyOps:
     def _vals(k: np.ndarray):
         return k if k.dtype == np.float64 else k.astype(np.float64)
 
-    def local_moments(self, keys, shift):
+    def local_moments(self, keys):
         k = keys.numpy()
         if k.size == 0:
-            return torch.zeros(3, dtype=torch.float64), torch.tensor([-1, 0], dtype=torch.int64)
-        d = self._vals(k) - shift
+            return torch.zeros(4, dtype=torch.float64), torch.tensor([-1, 0], dtype=torch.int64)
+        c = float(self._vals(k[:1])[0])
+        d = self._vals(k) - c
         o = O.ordered_u64(k)
-        return (torch.tensor([float(k.size), float(d.sum()), float((d * d).sum())], dtype=torch.float64),
+        return (torch.tensor([float(k.size), float(d.sum()), float((d * d).sum()), c], dtype=torch.float64),
                 torch.tensor(np.array([o.min(), o.max()], np.uint64).view(np.int64)))
 
     @staticmethod
@@ -183,6 +184,59 @@ def gloo_worker(rank, world, port, keys_all, pay_all, out_dir, k):
         ok, op, info = dist_zsort(keys, pay, lo, ops=NumpyOps(), k=k)
         np.save(os.path.join(out_dir, f"k{rank}.npy"), ok.numpy())
         np.save(os.path.join(out_dir, f"p{rank}.npy"), op.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+class StagedComm:
+    """dist.TorchComm over gloo for CUDA tensors: every collective copies its
+    operands to host memory, runs the gloo collective there and copies the
+    result back (gloo has no CUDA all_to_all).  Lets real processes run the
+    product DeviceOps path on one GPU without kernels that wait on another
+    process."""
+
+    def __init__(self):
+        from paper_2605_14419_b200.dist import TorchComm
+
+        self.inner = TorchComm()
+        self.world, self.rank = self.inner.world, self.inner.rank
+
+    def all_reduce(self, t, op):
+        h = t.cpu()
+        self.inner.all_reduce(h, op)
+        t.copy_(h)
+        return t
+
+    def all_gather(self, t):
+        return [x.to(t.device) for x in self.inner.all_gather(t.cpu())]
+
+    def all_to_all_single(self, out, inp, out_splits=None, in_splits=None):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        self.inner.all_to_all_single(h, inp.cpu(), out_splits, in_splits)
+        out.copy_(h)
+
+
+def gloo_device_worker(rank, world, port, keys_all, pay_all, out_dir, k):
+    """torch.multiprocessing target: one process per rank on cuda:0 running
+    dist_zsort with the product DeviceOps (CUDA kernels through the C ABI)
+    and TorchComm over gloo (staged through host memory)."""
+    import torch.distributed as dist
+
+    from paper_2605_14419_b200.dist import DeviceOps, dist_zsort
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        n = keys_all.size
+        lo, hi = rank * n // world, (rank + 1) * n // world
+        keys = torch.from_numpy(np.ascontiguousarray(keys_all[lo:hi])).to(dev)
+        pay = torch.from_numpy(np.ascontiguousarray(pay_all[lo:hi])).to(dev)
+        ok, op, info = dist_zsort(keys, pay, lo, ops=DeviceOps(dev), comm=StagedComm(), k=k)
+        np.save(os.path.join(out_dir, f"k{rank}.npy"), ok.cpu().numpy())
+        np.save(os.path.join(out_dir, f"p{rank}.npy"), op.cpu().numpy())
     finally:
         dist.destroy_process_group()
 

@@ -17,7 +17,7 @@ import pytest
 import torch
 
 from oracle import oracle as O
-from tests.dist_testlib import NumpyOps, config5_small, gloo_worker, run_threads
+from tests.dist_testlib import NumpyOps, config5_small, gloo_device_worker, gloo_worker, run_threads
 
 INT64_MIN, INT64_MAX = -(2**63), 2**63 - 1
 
@@ -118,4 +118,31 @@ def test_simulated_ranks_gpu(world):
     outs = run_threads(shards_of(keys, world, dev), lambda: DeviceOps(dev), k=4096)
     sizes = [o[0].numel() for o in outs]
     assert max(sizes) - min(sizes) <= 1, sizes  # exact cuts
+    check(keys, outs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["config5_recipe", "normal_f64", "heavy_run", "signed_zeros"])
+def test_two_processes_device_ops_gloo(name):
+    """The product distributed path in real processes: two ranks on cuda:0,
+    DeviceOps (CUDA kernels through the C ABI: D1 moments, D2 histograms and
+    cut refinement, the device occurrence search, the MODE_DEST partition,
+    the local sort) with TorchComm over gloo, collectives staged through host
+    memory.  No kernel of one process waits on the other."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    keys = dict(datasets())[name]
+    if name == "config5_recipe":
+        keys = config5_small(1 << 20)
+    pay = np.arange(keys.size, dtype=np.int64)
+    with tempfile.TemporaryDirectory() as td:
+        mp.start_processes(gloo_device_worker, args=(2, _free_port(), keys, pay, td, 4096), nprocs=2, join=True,
+                           start_method="spawn")
+        outs = [(torch.from_numpy(np.load(f"{td}/k{r}.npy")), torch.from_numpy(np.load(f"{td}/p{r}.npy")))
+                for r in range(2)]
+    sizes = [o[0].numel() for o in outs]
+    if name in ("config5_recipe", "heavy_run"):
+        assert max(sizes) - min(sizes) <= 1, sizes  # exact cuts, the long run split by position
     check(keys, outs)
