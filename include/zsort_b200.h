@@ -223,6 +223,12 @@ int32_t zsb_timing_read(double *ms, int64_t *launches, int32_t nslots, int32_t r
 /* Thread-local message for the last failing call. */
 const char *zsb_last_error(void);
 
+/* Bounds-check builds (-DZSB_CHECKS, tools/bounds_check.py): the number of
+ * out-of-range shared/global indices the data-path kernels have seen on this
+ * device since the last reset (synchronises the device); -1 in normal
+ * builds. */
+int64_t zsb_check_violations(int32_t reset);
+
 /* Build/version string (compile flags and target arch). */
 const char *zsb_version(void);
 

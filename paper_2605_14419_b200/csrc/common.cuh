@@ -11,6 +11,22 @@
 
 namespace zsb {
 
+// Bounds-check build (-DZSB_CHECKS; tools/bounds_check.py): every shared and
+// global index of the data path is range-checked and violations are counted
+// in zsb_check_count (read by zsb_check_violations()).  compute-sanitizer is
+// not available on this GPU pool; this is its stand-in.  Empty otherwise.
+#ifdef ZSB_CHECKS
+__device__ unsigned long long zsb_check_count;
+#define ZSB_CHECK(cond)                                         \
+    do {                                                        \
+        if (!(cond)) atomicAdd(&::zsb::zsb_check_count, 1ull); \
+    } while (0)
+#else
+#define ZSB_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 constexpr uint64_t SIGN = 0x8000000000000000ull;
 constexpr uint64_t ORD_PINF = 0xFFF0000000000000ull;  // ord_key<KEY_F64>(+inf); positive NaNs order above
 constexpr uint64_t ORD_NINF = 0x000FFFFFFFFFFFFFull;  // ord_key<KEY_F64>(-inf); negative NaNs order below
@@ -26,6 +42,8 @@ enum SegMode : int32_t {
     MODE_DEST = 3,     // multi-GPU exchange: bucket = destination rank from the global cuts
     MODE_ZCDF = 4,     // level 1, fitted: z-score coordinate through the piecewise-linear empirical CDF
                        // (histogram equalisation over kf coarse z-bins) -> equal-population buckets
+    MODE_ZLIN = 5,     // recursion levels, fitted: Eq. 1's line in fp32, fmaf((float)(x - center), za, zb)
+                       // (monotone; no fp64 division per key)
 };
 
 // Global cuts of the multi-GPU exchange (paper_2605_14419_b200/dist.py).
@@ -216,16 +234,30 @@ __device__ __forceinline__ int32_t bucket_cdf(double x, const SegParams &p, cons
     return bi < p.k ? bi : p.k - 1;
 }
 
-// BM = 1: the caller guarantees MODE_ZCDF (the level-1 kernels dispatch on the
-// mode once per CTA, so the hot loop carries one mapping, not four).
+// BM = 1: the caller guarantees MODE_ZCDF, BM = 3: MODE_ZSCORE (the kernels
+// dispatch on the segment's mode once per CTA, so the hot loop carries one
+// mapping, not five).
 template <int KK, int BM = 0>
 __device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p, int64_t pos = 0,
                                               const DestCuts *cuts = nullptr, const float2 *cdf = nullptr) {
-    if (BM == 1 || p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
-    if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
-    if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
-    if (p.mode == MODE_DEST) return dest_of<KK>(bits, pos, cuts);
-    return 0;
+    auto zlin = [&]() -> int32_t {
+        const float f = floorf(zc_coord(key_value<KK>(bits), p.center, p.za, p.zb));
+        return !(f > 0.0f) ? 0 : (f >= (float)p.k ? p.k - 1 : (int32_t)f);
+    };
+    if constexpr (BM == 1) {
+        return bucket_cdf(key_value<KK>(bits), p, cdf);
+    } else if constexpr (BM == 3) {
+        return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
+    } else if constexpr (BM == 4) {
+        return zlin();
+    } else {
+        if (p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
+        if (p.mode == MODE_ZLIN) return zlin();
+        if (p.mode == MODE_ZSCORE) return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
+        if (p.mode == MODE_INTEGER) return (int32_t)((ord_key<KK>(bits) - p.umin) >> p.shift);
+        if (p.mode == MODE_DEST) return dest_of<KK>(bits, pos, cuts);
+        return 0;
+    }
 }
 
 // ---------------------------------------------------------- warp helpers

@@ -22,6 +22,12 @@ namespace cg = cooperative_groups;
 namespace zsb {
 
 constexpr int NT = 256;        // threads per CTA for the streaming kernels
+#ifndef ZSB_BM_ZSCORE
+#define ZSB_BM_ZSCORE 1  // z-score segments (recursion levels) run a body specialised to Eq. 1
+#endif
+#ifndef ZSB_ZLIN
+#define ZSB_ZLIN 1  // fitted recursion levels map with Eq. 1's line in fp32 (MODE_ZLIN, own body)
+#endif
 constexpr int NWARPS = NT / 32;
 #ifndef ZSB_SCAN_ITEMS
 #define ZSB_SCAN_ITEMS 16
@@ -39,6 +45,7 @@ struct Buffers {
     const DestCuts *cuts;  // MODE_DEST only
     const float2 *cdf;     // MODE_ZCDF only: kf knot pairs (cdf[s], cdf[s+1]) in bucket units (staged in smem)
     unsigned long long *status;  // ZSB_ERR_NAN is raised here by a finish run holding a NaN (nullable)
+    int64_t n;                   // records (bounds of every buffer above; ZSB_CHECKS)
 };
 
 __device__ __forceinline__ const uint64_t *src_keys(const Buffers &B, int src) {
@@ -388,6 +395,17 @@ __global__ void k_seg_params(SegParams *segs, int nseg, const SegAcc *acc, MapCf
     SegParams p = segs[s];
     if (p.mode == MODE_COPY) return;
     finalize_params<KK>(p, acc[s].s2 / (double)p.len, acc[s].omin, acc[s].omax, mc, ctrl);
+    if (ZSB_ZLIN && mc.mapping == 0 && p.mode == MODE_ZSCORE) {
+        // fitted recursion: h = (x - center) * scale / std + zmin * scale as fp32 after one rounded
+        // fp64 subtraction -- monotone in x (every step is a rounded monotone map), so the final
+        // order is unchanged; paper mode keeps the exact Eq. 1 (one fp64 division per key)
+        const float za = (float)(p.scale / p.std), zb = (float)(p.zmin * p.scale);
+        if (za > 0.0f && za < 3.0e38f && fabsf(zb) < 3.0e38f) {
+            p.za = za;
+            p.zb = zb;
+            p.mode = MODE_ZLIN;
+        }
+    }
     segs[s] = p;
 }
 
@@ -449,11 +467,19 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
     bool nan = false;
     auto count = [&](uint64_t b, int64_t i) {
         if (screen) nan |= __longlong_as_double((long long)b) != __longlong_as_double((long long)b);
-        atomicAdd(&hist[seg_bucket<KK, BM>(b, p, i, B.cuts, cdf)], 1u);
+        const int bk = seg_bucket<KK, BM>(b, p, i, B.cuts, cdf);
+        ZSB_CHECK(bk >= 0 && bk < p.k);
+        atomicAdd(&hist[bk], 1u);
     };
     const uint64_t *tsrc = src + t0;
-    const int64_t len = t1 - t0;
-    if (stage_ok && ((uintptr_t)tsrc & 15) == 0) {
+    int64_t len = t1 - t0;
+    if (stage_ok && ((uintptr_t)tsrc & 15) != 0 && len > 0) {  // 8-byte head before the 16-byte-aligned copies
+        if (threadIdx.x == 0) count(__ldcs(tsrc), t0);
+        tsrc++;
+        t0++;
+        len--;
+    }
+    if (stage_ok) {
         uint64_t *ring = (uint64_t *)((unsigned char *)hist + (((size_t)((p.k + 1) & ~1) * 4 + (size_t)CDF_KNOTS * 8 + 127) &
                                                                 ~(size_t)127));
         const int nch = (int)((len + HIST_CHUNK - 1) / HIST_CHUNK);
@@ -508,13 +534,22 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
     for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
 }
 
-template <int KK>
+// L1: level-1 launch (bodies: CDF mapping, generic); else recursion levels
+// (bodies: Eq. 1, its fp32 line, generic).  One kernel per group keeps each
+// hot loop's code and registers to the mappings it can meet (measured on
+// B200: every extra body in one kernel cost the 10^7-key scatter ~3 %).
+template <int KK, int L1>
 __global__ void __launch_bounds__(HT) k_hist(Buffers B, const SegParams *__restrict__ segs, int nseg,
                                              uint32_t *__restrict__ mat, unsigned long long *status, int stage_ok,
                                              unsigned long long *scan_status, int scan_words,
                                              unsigned long long *ctrl) {
-    if (segs[find_seg(segs, nseg, blockIdx.x)].mode == MODE_ZCDF)
+    const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
+    if (L1 && mode == MODE_ZCDF)
         hist_body<KK, 1>(B, segs, nseg, mat, status, stage_ok, scan_status, scan_words, ctrl);
+    else if (!L1 && ZSB_BM_ZSCORE && mode == MODE_ZSCORE)
+        hist_body<KK, 3>(B, segs, nseg, mat, status, stage_ok, scan_status, scan_words, ctrl);
+    else if (!L1 && ZSB_ZLIN && mode == MODE_ZLIN)
+        hist_body<KK, 4>(B, segs, nseg, mat, status, stage_ok, scan_status, scan_words, ctrl);
     else
         hist_body<KK, 0>(B, segs, nseg, mat, status, stage_ok, scan_status, scan_words, ctrl);
 }
@@ -841,6 +876,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             if (FULL || i < prev_nvalid) {
                 const int b = stb[i];
                 const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
+                ZSB_CHECK(b < k && (int64_t)dst >= p.start && (int64_t)dst < p.start + p.len);
                 // evict_last: the runs (and the finish's input) stay in L2
                 st_keep(dk + dst, stk[i], l2pol);
                 if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
@@ -860,6 +896,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             if (FULL || pk[j] != 0xffffffffu) {
                 const int b = (int)(pk[j] & 0xFFFFu);
                 const uint32_t pos = (uint32_t)cnt[w * k + b] + (pk[j] >> 16);
+                ZSB_CHECK(b < k && pos < (uint32_t)ROUND);
                 stk[pos] = key[j];
                 if constexpr (PB != 0) stp[pos] = pay[j];
                 stb[pos] = (uint16_t)b;
@@ -891,6 +928,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         for (int i = threadIdx.x; i < prev_nvalid; i += ST) {
             const int b = stb[i];
             const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
+            ZSB_CHECK(b < k && (int64_t)dst >= p.start && (int64_t)dst < p.start + p.len);
             st_keep(dk + dst, stk[i], l2pol);
             if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
         }
@@ -903,12 +941,17 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
 #undef SCAT_MARK
 }
 
-template <int KK, int PB, int SW, int NSET>
+template <int KK, int PB, int SW, int NSET, int L1>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
                                                               int dst_sel, long long *prof) {
-    if (segs[find_seg(segs, nseg, blockIdx.x)].mode == MODE_ZCDF)
+    const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
+    if (L1 && mode == MODE_ZCDF)
         scatter_body<KK, PB, SW, 1, NSET>(B, segs, nseg, mat, dst_sel, prof);
+    else if (!L1 && ZSB_BM_ZSCORE && mode == MODE_ZSCORE)
+        scatter_body<KK, PB, SW, 3, NSET>(B, segs, nseg, mat, dst_sel, prof);
+    else if (!L1 && ZSB_ZLIN && mode == MODE_ZLIN)
+        scatter_body<KK, PB, SW, 4, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else
         scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof);
 }
@@ -1757,6 +1800,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
 
     const int m = e.len;
     if (m <= 0) return;
+    ZSB_CHECK(m <= cap && e.start >= 0 && e.start + m <= B.n);
     const uint64_t *sk = src_keys(B, e.src) + e.start;
     const P *sp = src_pay<PB>(B, e.src) + e.start;
     uint64_t *ok = B.out_k + e.start;
@@ -1991,6 +2035,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
                 const uint32_t old = atomicAdd(&cw[d >> 1], 1u << (16 * (d & 1)));
                 const uint32_t pos = (old >> (16 * (d & 1))) & 0xFFFFu;
                 const uint32_t ri = (uint32_t)(base + j * 32);
+                ZSB_CHECK(d < S && pos < (uint32_t)m && ri < (uint32_t)m);
                 if constexpr (decltype(pk_t)::value) {
                     Bo[pos] = ((o[j] - omin) << IB) | ri;
                 } else {
@@ -2070,6 +2115,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
             b0 = __shfl_sync(0xffffffffu, b0, leader);
             if (sl >= 0) {
                 const uint32_t pos = b0 + __popc(peers & lt);
+                ZSB_CHECK(pos < (uint32_t)m);
                 const uint32_t ri = (uint32_t)(base + j * 32);
                 if (packed) {
                     Bo[pos] = ((o[j] - omin) << IB) | ri;
@@ -2129,6 +2175,7 @@ __device__ __forceinline__ void finish_entry(const Buffers &B, const Entry e, in
                     refine[r] = Entry{e.start + a, c, 2};
                 }
             }
+            ZSB_CHECK(a + rank >= 0 && a + rank < m && idx >= 0 && idx < m && z <= m);
             ok[a + rank] = key_out(ov, idx);
             if constexpr (PB != 0) op[a + rank] = pin[idx];
         }
@@ -2281,6 +2328,7 @@ __device__ __forceinline__ int team_run(const Buffers &B, const Entry e, int cap
     const unsigned lt = lanemask_lt();
     const int r = (int)cl.block_rank();
     const int m = e.len;
+    ZSB_CHECK(m > 0 && m <= TEAM * cap && e.start >= 0 && e.start + m <= B.n);
     const int q = (m + TEAM - 1) / TEAM;
     const int c0 = min(m, r * q), mc = min(m, c0 + q) - c0;
     const uint64_t *kin = nullptr;
@@ -2448,6 +2496,7 @@ __device__ __forceinline__ int team_run(const Buffers &B, const Entry e, int cap
         c = __shfl_sync(0xffffffffu, c, leader);
         if (valid) {
             const uint32_t pos = ts.pbase[p] + c + (uint32_t)__popc(mm & lt);
+            ZSB_CHECK(p < TEAM_PARTS && pos < (uint32_t)m && pos >= ts.pstart[p] && pos < ts.pstart[p + 1]);
             st_keep(ok + pos, kin[i], l2pol);
             if constexpr (PB != 0) st_keep(op + pos, pin[i], l2pol);
         }

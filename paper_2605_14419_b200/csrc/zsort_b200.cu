@@ -115,6 +115,9 @@ void timing_collect() {
 #ifndef ZSB_TEAM_L1
 #define ZSB_TEAM_L1 0  // 1: level-1 buckets up to TEAM * cap are team runs (k sized for them); measured slower
 #endif
+#ifndef ZSB_HIST_RING_ALL
+#define ZSB_HIST_RING_ALL 0  // 1: recursion-level histograms also stage keys through the TMA ring (measured C4 +2 %)
+#endif
 #ifndef ZSB_K1_TEAM
 #define ZSB_K1_TEAM 2048  // cap on the level-1 bucket count when buckets are sized for team runs
 #endif
@@ -399,21 +402,20 @@ int fin_prefetch(int64_t n, int pb) {
     return (double)n * (8 + pb) > 128.0 * (1 << 20) ? 1 : 0;
 }
 
-template <int KK, int PB>
-int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
+template <int KK, int PB, int L1>
+int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
                      bool segs_level1 = false, cudaEvent_t after_scan = nullptr) {
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
-    // the TMA ring pays off on long tiles (level 1); short recursion tiles run
-    // several CTAs per SM without it
-    const bool ring = segs_level1;
+    // keys through the TMA ring on every level (recursion tiles: 8-32 K keys)
+    const bool ring = segs_level1 || ZSB_HIST_RING_ALL;
     const size_t kbytes = hist_smem(kmax, ring);
-    smem_optin(k_hist<KK>, kbytes);
+    smem_optin(k_hist<KK, L1>, kbytes);
     const int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
     {
         PhaseScope ph(PH_HIST, c.st);
-        k_hist<KK><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, ring ? 1 : 0, status,
+        k_hist<KK, L1><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, ring ? 1 : 0, status,
                                                          (int)(sblocks + 1), ctrl);
     }
     ZSB_LAUNCH("k_hist");
@@ -432,25 +434,33 @@ int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t m
                                        : (scat_layout(kmax, PB, 16, 1).total + cdf_bytes <= smax ? 1 : 0));
     if (nset16 == 0) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
-        smem_optin(k_scatter<KK, PB, 8, 2>, sbytes);
+        smem_optin(k_scatter<KK, PB, 8, 2, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 8, 2><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
+        k_scatter<KK, PB, 8, 2, L1><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
                                                                         scat_prof(tiles));
     } else if (nset16 == 2) {
         const size_t sbytes = scat_layout(kmax, PB, 16, 2).total + cdf_bytes;
-        smem_optin(k_scatter<KK, PB, 16, 2>, sbytes);
+        smem_optin(k_scatter<KK, PB, 16, 2, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 16, 2><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
+        k_scatter<KK, PB, 16, 2, L1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
                                                                          scat_prof(tiles));
     } else {
         const size_t sbytes = scat_layout(kmax, PB, 16, 1).total + cdf_bytes;
-        smem_optin(k_scatter<KK, PB, 16, 1>, sbytes);
+        smem_optin(k_scatter<KK, PB, 16, 1, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter<KK, PB, 16, 1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
+        k_scatter<KK, PB, 16, 1, L1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
                                                                          scat_prof(tiles));
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
+}
+
+template <int KK, int PB>
+int launch_partition(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
+                     bool segs_level1 = false, cudaEvent_t after_scan = nullptr) {
+    return segs_level1 ? launch_partition_l<KK, PB, 1>(c, segs, nseg, tiles, mat_entries, kmax, dst_sel, true, after_scan)
+                       : launch_partition_l<KK, PB, 0>(c, segs, nseg, tiles, mat_entries, kmax, dst_sel, false,
+                                                       after_scan);
 }
 
 #ifdef ZSB_PHASE_PROFILE
@@ -998,6 +1008,7 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     ctx.B.cuts = nullptr;
     ctx.B.cdf = nullptr;
     ctx.B.status = nullptr;
+    ctx.B.n = n;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0],
@@ -1049,6 +1060,22 @@ struct PartitionOp {
 extern "C" {
 
 const char *zsb_last_error(void) { return g_err.c_str(); }
+
+int64_t zsb_check_violations(int32_t reset) {
+#ifdef ZSB_CHECKS
+    unsigned long long h = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&h, zsb_check_count, sizeof(h));
+    if (reset) {
+        const unsigned long long z = 0;
+        cudaMemcpyToSymbol(zsb_check_count, &z, sizeof(z));
+    }
+    return (int64_t)h;
+#else
+    (void)reset;
+    return -1;  // not a bounds-check build
+#endif
+}
 
 void zsb_timing_enable(int32_t on) {
     g_t.on = on != 0;
@@ -1116,6 +1143,7 @@ int sort_entry(const void *d_keys, int32_t key_dtype, const void *d_payload, int
     ctx.B.cuts = nullptr;
     ctx.B.cdf = (const float2 *)(ctx.ws + ctx.L.lut);
     ctx.B.status = (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS;
+    ctx.B.n = n;
     return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats, rec);
 }
 }  // namespace
@@ -1198,13 +1226,13 @@ int zsb_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const double
     uint32_t *mat = (uint32_t *)(ctx.ws + ctx.L.mat);
     size_t kb = (size_t)k * 4;
     if (key_dtype == ZSB_KEY_I64) {
-        smem_optin(k_hist<0>, kb);
-        k_hist<0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
+        smem_optin(k_hist<0, 0>, kb);
+        k_hist<0, 0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
                                                            (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0,
                                                            nullptr, 0, nullptr);
     } else {
-        smem_optin(k_hist<1>, kb);
-        k_hist<1><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
+        smem_optin(k_hist<1, 0>, kb);
+        k_hist<1, 0><<<(unsigned)ctx.P.ntiles, HT, kb, ctx.st>>>(ctx.B, seg, 1, mat,
                                                            (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS, 0,
                                                            nullptr, 0, nullptr);
     }
@@ -1479,6 +1507,7 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ctx.B.cuts = dc;
     ctx.B.cdf = nullptr;
     ctx.B.status = nullptr;
+    ctx.B.n = n;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     count_launches(1);

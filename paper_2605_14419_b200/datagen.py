@@ -127,3 +127,41 @@ def _swap_pairs(arr, pairs):
         a[i], a[j] = aj, ai
         start += take
     return a.cpu().numpy()
+
+
+# ------------------------------------------------- device family generator
+# The reference's key families (datagen.py:92-162: uniform, normal, skewed,
+# nearly_sorted, high_duplicate) drawn on the device by the library's
+# counter-based generator (zsb_generate, csrc/gen_kernels.cuh): key i is a
+# pure function of (family, seed, i, params), so 10^8-10^9-key workloads are
+# built in HBM in milliseconds and any shard can be regenerated.
+
+FAMILIES = ("uniform", "normal", "skewed", "nearly_sorted", "high_duplicate")
+FAMILY_DEFAULTS = {"normal_mu": 0.0, "normal_sigma": 1e9, "pareto_alpha": 1.5, "pareto_xm": 1.0,
+                   "swap_fraction": 0.01, "dup_range": 1000}  # the reference's DistributionSpec defaults
+
+
+def device_family(kind: str, n: int, seed: int = 1, offset: int = 0, n_total: int | None = None,
+                  device="cuda", **params) -> torch.Tensor:
+    """int64 keys of positions [offset, offset + n) of an n_total-key workload
+    of family ``kind`` (defaults of the reference's DistributionSpec unless
+    overridden), generated on ``device`` by the CUDA kernel."""
+    import ctypes
+
+    from . import _lib
+
+    if kind not in FAMILIES:
+        raise ValueError(f"unknown family {kind!r}; one of {FAMILIES}")
+    unknown = set(params) - set(FAMILY_DEFAULTS)
+    if unknown:
+        raise TypeError(f"unknown family parameters {sorted(unknown)}")
+    p = dict(FAMILY_DEFAULTS, **params)
+    n_total = n if n_total is None else n_total
+    out = torch.empty(n, dtype=torch.int64, device=device)
+    arr = (ctypes.c_double * 6)(p["normal_mu"], p["normal_sigma"], p["pareto_alpha"], p["pareto_xm"],
+                                p["swap_fraction"], float(p["dup_range"]))
+    L = _lib.load()
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    _lib.check(L.zsb_generate(FAMILIES.index(kind), int(offset), int(n), int(n_total),
+                              ctypes.c_uint64(seed & ((1 << 64) - 1)), arr, out.data_ptr(), stream))
+    return out
