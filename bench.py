@@ -396,8 +396,17 @@ def e2e_leg(Z, keys_h, pay_h, cfg, S, flush, stream, steps):
     e2e_step = sum(e2e_ms) / len(e2e_ms)
     if not (np.array_equal(hok.numpy(), S.out_k.cpu().numpy()) and np.array_equal(hop.numpy(), S.out_p.cpu().numpy())):
         raise SystemExit("e2e output differs from the device-resident run")
+    # the copies alone (same pinned buffers, same sizes): every output key
+    # depends on every input key, so no output can leave before the last input
+    # has arrived -- H2D + D2H is the floor of an end-to-end sort over PCIe
+    dk, dp = torch.empty(hk.shape, dtype=hk.dtype, device="cuda"), torch.empty(hp.shape, dtype=hp.dtype, device="cuda")
+    h2d = timed_steps(lambda: (dk.copy_(hk, non_blocking=True), dp.copy_(hp, non_blocking=True)), 3, flush, stream)
+    d2h = timed_steps(lambda: (hok.copy_(dk, non_blocking=True), hop.copy_(dp, non_blocking=True)), 3, flush, stream)
+    copy_floor = min(h2d) + min(d2h)
     return {"value": n / (e2e_step / 1e3), "unit": "keys/s", "h2d_bytes_per_step": int(n * rec),
             "d2h_bytes_per_step": int(n * rec), "ms_per_step": e2e_step,
+            "copy_floor_ms": copy_floor, "h2d_gbs": n * rec / min(h2d) / 1e6, "d2h_gbs": n * rec / min(d2h) / 1e6,
+            "vs_copy_floor": e2e_step / copy_floor,
             "api": "paper_2605_14419_b200.zsort(pinned host tensors, out=pinned host tensors)"}
 
 

@@ -132,7 +132,8 @@ enum Ctrl {
     C_FTICK3 = 23,
     C_NTEAM = 24,        // team runs of the level (cap < len <= TEAM * cap)
     C_TTICK = 25,        // team run ticket
-    C_SLOTS = 26
+    C_NEED_STATS = 26,   // some child of the level needs the moments pass (k_seg_moments) before its mapping
+    C_SLOTS = 27
 };
 
 // ------------------------------------------------------------ key traits

@@ -393,7 +393,7 @@ __global__ void k_seg_params(SegParams *segs, int nseg, const SegAcc *acc, MapCf
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nseg) return;
     SegParams p = segs[s];
-    if (p.mode == MODE_COPY) return;
+    if (p.mode == MODE_COPY || p.mode == MODE_ZLIN) return;  // ZLIN: ranged by the level-1 CDF (classify)
     finalize_params<KK>(p, acc[s].s2 / (double)p.len, acc[s].omin, acc[s].omax, mc, ctrl);
     if (ZSB_ZLIN && mc.mapping == 0 && p.mode == MODE_ZSCORE) {
         // fitted recursion: h = (x - center) * scale / std + zmin * scale as fp32 after one rounded
@@ -445,6 +445,7 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
             ctrl[C_NENTRY] = 0ull;
             ctrl[C_NTEAM] = 0ull;
             ctrl[C_TTICK] = 0ull;
+            ctrl[C_NEED_STATS] = 0ull;
         }
     }
     int s = find_seg(segs, nseg, blockIdx.x);
@@ -471,6 +472,7 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
         ZSB_CHECK(bk >= 0 && bk < p.k);
         atomicAdd(&hist[bk], 1u);
     };
+
     const uint64_t *tsrc = src + t0;
     int64_t len = t1 - t0;
     if (stage_ok && ((uintptr_t)tsrc & 15) != 0 && len > 0) {  // 8-byte head before the 16-byte-aligned copies
@@ -503,12 +505,12 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
             const int clen = (int)min((int64_t)HIST_CHUNK, len - c0);
             const uint64_t *kb = ring + (size_t)st * HIST_CHUNK;
             const int cfull = clen & ~1;  // an odd last key is outside the 16-byte copy
-            if (clen == HIST_CHUNK) {  // full chunk: fixed trip count, loads first
+            if (clen == HIST_CHUNK) {  // full chunk: fixed trip count, loads first, then buckets, then atomics
                 constexpr int PER = HIST_CHUNK / HT;
                 uint64_t kv[PER];
 #pragma unroll
                 for (int u = 0; u < PER; u++) kv[u] = kb[threadIdx.x + u * HT];
-#pragma unroll
+                #pragma unroll
                 for (int u = 0; u < PER; u++) count(kv[u], t0 + c0 + threadIdx.x + u * HT);
             } else {
 #pragma unroll 4
@@ -525,7 +527,7 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
             uint64_t b[8];
 #pragma unroll
             for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
-#pragma unroll
+            #pragma unroll
             for (int u = 0; u < 8; u++) count(b[u], i + u * HT);
         }
         for (; i < t1; i += HT) count(__ldcs(src + i), i);
@@ -713,6 +715,48 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
     const int tid = threadIdx.x, w = tid >> 5, lane = lane_id();
     const int per = (ndig + T - 1) / T;
     const int d0 = min(ndig, tid * per), d1 = min(ndig, d0 + per);
+    if ((per == 2 || per == 4) && ndig == per * T) {
+        // packed path (k = 2T or 4T, the level-1 fan-outs): a thread's digit
+        // pairs are u32 words of every warp's row; both digits of a pair
+        // advance together in one packed add (counts and positions stay below
+        // 2^16), and the rows are re-read in the write-back rather than held
+        // in registers (the round's keys and ranks are live here)
+        const int np = per >> 1;
+        uint32_t *c32 = (uint32_t *)cnt;
+        uint32_t ps0 = 0, ps1 = 0;
+#pragma unroll
+        for (int ww = 0; ww < SW; ww++) ps0 += c32[(ww * ndig + d0) >> 1];
+        if (np == 2)
+#pragma unroll
+            for (int ww = 0; ww < SW; ww++) ps1 += c32[((ww * ndig + d0) >> 1) + 1];
+        const uint32_t tsum = (ps0 & 0xFFFFu) + (ps0 >> 16) + (ps1 & 0xFFFFu) + (ps1 >> 16);
+        uint32_t x = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        uint32_t run = x - tsum + warps_before(wsum, w, lane);
+        for (int q = 0; q < np; q++) {
+            const uint32_t ps = q ? ps1 : ps0;
+            const uint32_t lo = run, hi = run + (ps & 0xFFFFu);
+            uint32_t r = lo | (hi << 16);
+            *(uint32_t *)(dstart + d0 + 2 * q) = r;
+#pragma unroll
+            for (int ww = 0; ww < SW; ww++) {
+                uint32_t *a = c32 + ((ww * ndig + d0) >> 1) + q;
+                const uint32_t c = *a;
+                *a = r;
+                r += c;
+            }
+            run = hi + (ps >> 16);
+        }
+        if (tid == T - 1) dstart[ndig] = (uint16_t)run;
+        __syncthreads();
+        return;
+    }
     uint32_t tsum = 0;
     for (int d = d0; d < d1; d++)
 #pragma unroll
@@ -850,6 +894,10 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         // with no re-read, 27 % slower; a second __syncwarp between the atomic
         // and the re-read, 8 % slower.)
         uint32_t pk[ITEMS];  // bucket | rank << 16
+        // (Measured and not used: computing every item's bucket and the
+        // previous round's writes in a barrier-free loop before the ranking
+        // loop -- C4 scatter +11 %: the stores interleaved with the ranking
+        // chain are what hides their issue.)
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
             const int bkj = (FULL || base + j * 32 < nvalid)
@@ -1338,6 +1386,7 @@ struct ClassCfg {
     int32_t child_fill;  // recursion children: k = pow2 >= child_fill * len / kcap (buckets ~ kcap / child_fill)
     int32_t greedy;      // recursion levels pack finish runs greedily (else fixed windows)
     int32_t team_cap;    // buckets of cap < len <= team_cap are team runs (K5t); 0: none
+    int32_t child_from_cdf;  // children of the equalised level 1 take their range from its CDF (no moments pass)
 };
 
 __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64_t g) {
@@ -1353,6 +1402,22 @@ __device__ __forceinline__ int seg_of_slot(const int64_t *first, int nseg, int64
 // A value whose equalised bucket is b (approximately its middle): the knot
 // pair bracketing b + 0.5, linear inside the coarse bin, back through the
 // coarse coordinate.
+// The key value at equalised bucket coordinate t (t = b: the lower edge of
+// bucket b): the knot pair bracketing t, linear inside the coarse bin, back
+// through the coarse coordinate (the inverse of bucket_cdf up to rounding).
+__device__ inline double zcdf_at(const SegParams &p, const float2 *cdf, float t) {
+    int lo = 0, hi = p.kf - 1;  // first bin whose upper knot exceeds t
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cdf[mid].y <= t) lo = mid + 1;
+        else hi = mid;
+    }
+    const float2 az = cdf[lo];
+    float fr = az.y > az.x ? (t - az.x) / (az.y - az.x) : 0.0f;
+    fr = fminf(fmaxf(fr, 0.0f), 1.0f);
+    return p.center + ((double)lo + (double)fr - (double)p.zb) / (double)p.za;
+}
+
 __device__ inline double zcdf_inverse(const SegParams &p, const float2 *cdf, int b) {
     const float t = (float)b + 0.5f;
     int lo = 0, hi = p.kf - 1;  // first bin whose upper knot exceeds t
@@ -1397,10 +1462,33 @@ __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restri
     ch.level = p.level + 1;
     ch.src = (p.src == 1) ? 2 : 1;
     ch.k = p.k;
-    bool integer = p.mode == MODE_INTEGER || c == p.len || ch.level > cc.depth_guard;
+    // a parent ranged by the level-1 CDF (p.shift < 0: approximate extremes)
+    // whose bucket took every record gets the exact moments pass, not the
+    // integer fallback: all its keys may be equal (then MODE_COPY) or the
+    // estimate may have missed their range
+    const bool approx = p.mode == MODE_ZLIN && p.shift < 0;
+    bool integer = p.mode == MODE_INTEGER || (c == p.len && !approx) || ch.level > cc.depth_guard;
+    double lo = 0.0, hi = 0.0;
+    if (!integer && p.mode == MODE_ZCDF && cc.child_from_cdf) {
+        lo = zcdf_at(p, B.cdf, (float)b);
+        hi = zcdf_at(p, B.cdf, (float)(b + 1));
+    }
     if (integer) {
         ch.mode = MODE_INTEGER;
         atomicAdd(&ctrl[C_ST_FALLBACKS], 1ull);
+        atomicOr(&ctrl[C_NEED_STATS], 1ull);
+    } else if (p.mode == MODE_ZCDF && hi > lo && isfinite(lo) && isfinite(hi) && isfinite(hi - lo)) {
+        // a child of the equalised level 1 (fitted): the fitted line over the
+        // bucket's key range -- the level-1 CDF's inverse at the bucket's two
+        // edges -- needs no moments pass over its records (the line depends on
+        // min and max only; keys past the estimated edges clamp into the end
+        // buckets); scale and the fp32 coefficients follow from k (plan_block)
+        ch.mode = MODE_ZLIN;
+        ch.center = lo;
+        ch.std = hi - lo;
+        ch.zmin = 0.0;
+        ch.za = 0.0f;
+        ch.shift = -1;  // approximate range (see `approx`)
     } else if (p.mode == MODE_ZCDF) {
         // an equal-population bucket is not a z-interval: centre the child on
         // the inverse of the equalised map at the bucket's middle (any value
@@ -1408,9 +1496,11 @@ __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restri
         // scattered data, so classify can run beside the scatter)
         ch.mode = MODE_ZSCORE;
         ch.center = zcdf_inverse(p, B.cdf, b);
+        atomicOr(&ctrl[C_NEED_STATS], 1ull);
     } else {
         ch.mode = MODE_ZSCORE;
         ch.center = __dadd_rn(__dmul_rn(__dsub_rn(__ddiv_rn((double)b + 0.5, p.scale), p.zmin), p.std), p.center);
+        atomicOr(&ctrl[C_NEED_STATS], 1ull);
     }
     unsigned long long slot = atomicAdd(&ctrl[C_NCHILD], 1ull);
     children[slot] = ch;
@@ -1530,6 +1620,18 @@ __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, 
             int k = 16;
             while (k < want && k < kmax_child) k <<= 1;
             p.k = k;
+            if (p.mode == MODE_ZLIN && p.za == 0.0f) {  // a child ranged by the level-1 CDF: its fitted line
+                p.scale = (double)k * (1.0 - 0x1p-20);
+                const float za = (float)(p.scale / p.std);
+                if (za > 0.0f && za < 3.0e38f) {
+                    p.za = za;
+                    p.zb = 0.0f;
+                } else {  // degenerate range estimate: moments pass and Eq. 1 instead
+                    p.mode = MODE_ZSCORE;
+                    p.center = p.center + 0.5 * p.std;
+                    atomicOr(&ctrl[C_NEED_STATS], 1ull);
+                }
+            }
             int64_t tl = max((int64_t)min_tile, (int64_t)4 * k);
             tl = (tl + 255) & ~(int64_t)255;
             p.tile_len = tl;

@@ -115,6 +115,9 @@ void timing_collect() {
 #ifndef ZSB_TEAM_L1
 #define ZSB_TEAM_L1 0  // 1: level-1 buckets up to TEAM * cap are team runs (k sized for them); measured slower
 #endif
+#ifndef ZSB_CHILD_FROM_CDF
+#define ZSB_CHILD_FROM_CDF 1  // children of the equalised level 1 ranged by its CDF: no level-2 moments pass
+#endif
 #ifndef ZSB_HIST_RING_ALL
 #define ZSB_HIST_RING_ALL 0  // 1: recursion-level histograms also stage keys through the TMA ring (measured C4 +2 %)
 #endif
@@ -747,7 +750,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
               rec ? rec->scale : 0.0};
     ClassCfg cc{(int32_t)c.P.cap, (int32_t)c.P.half, (int32_t)cfg.depth_guard, cfg.mapping,
                 (int32_t)std::max(1, std::min(16, ZSB_CHILD_FILL)), ZSB_GREEDY,
-                0};
+                0, ZSB_CHILD_FROM_CDF};
     // team runs (K5t) finish the few oversized buckets of recursion levels,
     // which would otherwise cost whole extra levels (level 1: ZSB_TEAM_L1)
     const int32_t team_cap = team_grid<KK, PB>() > 0 ? (int32_t)(TEAM * c.P.cap) : 0;
@@ -806,13 +809,14 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
     int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
     int kmax = (int)c.P.k;
     int level = 1, par = 0;
+    bool need_stats = true;  // the next level's children need the moments pass (read from classify)
     if (rec) {  // the segment's own stats pass, then the level loop as for a recursion level
         SegAcc a0{~0ull, 0ull, 0.0, 0.0};
         ZSB_CUDA(cudaMemcpyAsync(acc, &a0, sizeof(a0), cudaMemcpyHostToDevice, c.st));
     }
     while (true) {
         cc.team_cap = (level > 1 || ZSB_TEAM_L1) ? team_cap : 0;
-        if (level > 1 || rec) {
+        if ((level > 1 && need_stats) || rec) {
             {
                 PhaseScope ph(PH_SEGSTATS, c.st, 2);
                 k_seg_moments<KK><<<(unsigned)tiles, NT, 0, c.st>>>(c.B, seg_cur, nseg, acc);
@@ -866,6 +870,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
         }
         stats[ZSB_STAT_INSERTION] += nentry;
         const int64_t nchild = (int64_t)hc[C_NCHILD];
+        need_stats = hc[C_NEED_STATS] != 0;
 #ifdef ZSB_DEBUG_LOG
         {  // host time since the call started: when this level's classify was seen
             static thread_local std::chrono::steady_clock::time_point t_call;
