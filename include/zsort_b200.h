@@ -20,10 +20,11 @@
  *  - reentrant: a call's state lives in its workspace;
  *    the library keeps only per-host-thread state (a pinned control-block
  *    mirror, two events and a side stream per thread, created at first use)
- *    and a once-per-device shared-memory opt-in guarded by a mutex, so
- *    concurrent calls from different host threads on their own streams and
- *    workspaces are independent (tests/test_gpu_parity.py::TestConcurrency);
- *    nothing reads the environment (tuning constants are compile-time);
+ *    and once-per-device kernel attributes (shared-memory opt-in, the team
+ *    kernel's resident-cluster count) guarded by mutexes, so concurrent
+ *    calls from different host threads on their own streams and workspaces
+ *    are independent (tests/test_gpu_contract.py::TestConcurrency); nothing
+ *    reads the environment (tuning constants are compile-time);
  *  - return 0 on success or a ZSB_ERR_* code; zsb_last_error() gives a
  *    thread-local message.  The Python wrapper maps ZSB_ERR_ARG/ZSB_ERR_NAN
  *    to ValueError and ZSB_ERR_DTYPE to TypeError, like core.py:151-181.

@@ -1697,6 +1697,30 @@ __device__ void plan_block(SegParams *segs, const unsigned long long *nseg_ptr, 
     }
 }
 
+// Finish order of a level's runs, longest first (64 length classes, any
+// order inside a class): the persistent finish takes runs by ticket, so the
+// last wave is short runs instead of whichever came last in key order.
+__device__ void order_runs(const Entry *entries, const unsigned long long *nentry_ptr, int32_t *order, int cap) {
+    constexpr int NCLS = 64;
+    __shared__ uint32_t ccount[NCLS];
+    const int ne = (int)*(volatile const unsigned long long *)nentry_ptr;
+    if (threadIdx.x < NCLS) ccount[threadIdx.x] = 0;
+    __syncthreads();
+    auto cls = [&](int i) { return NCLS - 1 - min(NCLS - 1, (int)((int64_t)entries[i].len * NCLS / (cap + 1))); };
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) atomicAdd(&ccount[cls(i)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int c = 0; c < NCLS; c++) {
+            const uint32_t v = ccount[c];
+            ccount[c] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) order[atomicAdd(&ccount[cls(i)], 1u)] = i;
+}
+
 // Classify, one cooperative launch (1024-thread CTAs, grid barriers): bucket
 // starts and child segments, then finish windows, then (CTA 0) the plan of
 // the next level -- which rewrites kfirst/wfirst, hence the second barrier.
@@ -1705,7 +1729,8 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
                                                    SegParams *children, SegAcc *acc, Entry *entries,
                                                    unsigned long long *ctrl, ClassCfg cc, int64_t total_slots,
                                                    int64_t total_windows, Buffers B, int key_kind, int32_t kmax_child,
-                                                   int32_t min_tile, unsigned long long *ref_zero, Entry *teams) {
+                                                   int32_t min_tile, unsigned long long *ref_zero, Entry *teams,
+                                                   int32_t *order) {
     cg::grid_group grid = cg::this_grid();
     if (blockIdx.x == 0 && threadIdx.x < 4 && ref_zero) ref_zero[threadIdx.x] = 0ull;  // the finish's refine counts/tickets
     const int64_t G = (int64_t)gridDim.x * blockDim.x, g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1754,6 +1779,7 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
     if (blockIdx.x == 0)
         plan_block(children, ctrl + C_NCHILD, kfirst, wfirst, ctrl, cc.cap, kmax_child, min_tile, cc.child_fill,
                    cc.team_cap > cc.cap ? cc.team_cap : cc.cap);
+    if (order && blockIdx.x == (gridDim.x > 1 ? 1 : 0)) order_runs(entries, ctrl + C_NENTRY, order, cc.cap);
 }
 
 // ------------------------------------------------------------------- K5
@@ -2321,7 +2347,7 @@ template <int KK, int PB>
 __device__ __forceinline__ void finish_list(const Buffers &B, const Entry *__restrict__ entries, int64_t ne, int cap,
                                             Entry *refine, unsigned long long *refine_count, int fin_ins,
                                             long long *prof, unsigned long long *ticket, int prefetch, uint64_t *bar,
-                                            uint32_t &parity) {
+                                            uint32_t &parity, const int32_t *order = nullptr) {
     __shared__ long long next, cur_s;
     long long cur = 0;
     if (threadIdx.x == 0) cur = (long long)atomicAdd(ticket, 1ull);
@@ -2329,14 +2355,15 @@ __device__ __forceinline__ void finish_list(const Buffers &B, const Entry *__res
         if (threadIdx.x == 0) {
             const long long nx = (long long)atomicAdd(ticket, 1ull);
             next = nx;
-            if (nx < ne && prefetch) finish_prefetch<PB>(B, entries[nx]);
+            if (nx < ne && prefetch) finish_prefetch<PB>(B, entries[order ? order[nx] : nx]);
         }
         if (threadIdx.x == 0) cur_s = cur;
         __syncthreads();
         const int64_t i = cur_s;
         cur = next;
         if (i >= ne) break;
-        finish_entry<KK, PB>(B, entries[i], i, cap, refine, refine_count, fin_ins, prof, bar, parity);
+        const int64_t ei = order ? order[i] : i;
+        finish_entry<KK, PB>(B, entries[ei], ei, cap, refine, refine_count, fin_ins, prof, bar, parity);
         __syncthreads();
     }
 }
@@ -2703,6 +2730,7 @@ __device__ void refine_loop(const Buffers &B, Entry *list_a, unsigned long long 
 }
 
 struct RefineArgs {  // the refine iterations a finish launch runs after its own list (list_b == nullptr: none)
+    const int32_t *order;  // finish order of the launch's own list (nullptr: list order)
     Entry *list_b;
     unsigned long long *count_b;
     int64_t cap_list;
@@ -2733,7 +2761,8 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
         if ((int64_t)blockIdx.x < ne) finish_entry<KK, PB>(B, entries[blockIdx.x], blockIdx.x, cap, refine, refine_count,
                                                            fin_ins, prof, bar, parity);
     } else {
-        finish_list<KK, PB>(B, entries, ne, cap, refine, refine_count, fin_ins, prof, ticket, prefetch, bar, parity);
+        finish_list<KK, PB>(B, entries, ne, cap, refine, refine_count, fin_ins, prof, ticket, prefetch, bar, parity,
+                            ra.order);
     }
     if (ra.list_b) {
         fence_proxy_async_global();  // refine runs are re-staged by TMA (async proxy) after the barrier
