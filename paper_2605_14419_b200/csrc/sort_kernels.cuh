@@ -665,6 +665,9 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 #endif
 constexpr int SCAT_ITEMS = ZSB_SCAT_ITEMS;
 constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
+#ifndef ZSB_SCAT_AHEAD
+#define ZSB_SCAT_AHEAD 0  // 1: each item's bucket computed one item ahead of its ranking (measured neutral)
+#endif
 // SW warps per CTA: 8 (4096-record rounds, two CTAs per SM) for k <= 1024,
 // 16 (8192-record rounds, one CTA per SM) above, so that a bucket's run in a
 // round stays >= 4 records = one 32-byte sector of keys (shorter runs leave
@@ -898,11 +901,22 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         // previous round's writes in a barrier-free loop before the ranking
         // loop -- C4 scatter +11 %: the stores interleaved with the ranking
         // chain are what hides their issue.)
+        auto bucket_of_item = [&](int j) -> int {
+            return (FULL || base + j * 32 < nvalid) ? seg_bucket<KK, BM>(key[j], p, r0 + base + j * 32, B.cuts, cdf)
+                                                    : -1;
+        };
+        // the next item's bucket (its mapping-table load) is computed ahead,
+        // before this item's warp barrier, so it overlaps the ranking chain
+        int bk_next = ZSB_SCAT_AHEAD ? bucket_of_item(0) : 0;
 #pragma unroll
         for (int j = 0; j < ITEMS; j++) {
-            const int bkj = (FULL || base + j * 32 < nvalid)
-                                ? seg_bucket<KK, BM>(key[j], p, r0 + base + j * 32, B.cuts, cdf)
-                                : -1;
+            int bkj;
+            if constexpr (ZSB_SCAT_AHEAD) {
+                bkj = bk_next;
+                if (j + 1 < ITEMS) bk_next = bucket_of_item(j + 1);
+            } else {
+                bkj = bucket_of_item(j);
+            }
             uint32_t old = 0, after = 0;
             const int q = w * k + (bkj < 0 ? 0 : bkj);
             const uint32_t sh = 16 * (q & 1);
