@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the paper-mapping and config-5 single-GPU legs")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="N>1: fused peer-store exchange or NCCL all_to_all (auto: p2p when peers are accessible)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -535,9 +537,29 @@ def run_dist(args, rank, world, dev):
     dp = torch.arange(base, base + n, dtype=torch.int64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    for _ in range(max(3, args.warmup)):
-        ok, op, info = dist_zsort(dk, dp, base)
-    torch.cuda.synchronize()
+    # the exchange: fused into the partition kernel (stores into the peers'
+    # receive buffers over NVLink) when every pair of the ranks' GPUs has peer
+    # access, else NCCL all_to_all; a failure of the fused path falls back
+    exchange = args.exchange
+    if exchange == "auto":
+        peer = torch.tensor([1 if all(torch.cuda.can_device_access_peer(dev.index, d)
+                                      for d in range(torch.cuda.device_count()) if d != dev.index) else 0],
+                            device=dev)
+        dist.all_reduce(peer, op=dist.ReduceOp.MIN)
+        exchange = "p2p" if int(peer.item()) else "nccl"
+    try:
+        for _ in range(max(3, args.warmup)):
+            ok, op, info = dist_zsort(dk, dp, base, exchange=exchange)
+        torch.cuda.synchronize()
+    except Exception as exc:  # keep the scaling run alive on the proven path
+        if exchange != "p2p":
+            raise
+        print(f"[bench] fused p2p exchange failed ({exc}); using nccl", file=sys.stderr, flush=True)
+        exchange = "nccl"
+        dist.barrier()
+        for _ in range(max(3, args.warmup)):
+            ok, op, info = dist_zsort(dk, dp, base, exchange=exchange)
+        torch.cuda.synchronize()
     # global correctness: per-rank structural check (keys regenerated from the
     # global index) and ordered boundaries between consecutive ranks
     viol = check_dist_output(Z, datagen, ok, op, n_total, dev)
@@ -558,7 +580,7 @@ def run_dist(args, rank, world, dev):
     with ClockSampler(dev.index) as clk:
         t_end = time.perf_counter() + 1.5
         while time.perf_counter() < t_end:
-            dist_zsort(dk, dp, base)
+            dist_zsort(dk, dp, base, exchange=exchange)
         torch.cuda.synchronize()
         for _ in range(args.steps):
             flush.zero_()
@@ -567,7 +589,7 @@ def run_dist(args, rank, world, dev):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ok, op, info = dist_zsort(dk, dp, base)
+            ok, op, info = dist_zsort(dk, dp, base, exchange=exchange)
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -588,7 +610,7 @@ def run_dist(args, rank, world, dev):
     for _ in range(args.steps):
         flush.zero_()
         dist.barrier()
-        dist_zsort(dk, dp, base)
+        dist_zsort(dk, dp, base, exchange=exchange)
     torch.cuda.synchronize()
     L.zsb_timing_enable(0)
     L.zsb_timing_read(ms_phase, launches, 8, 1)
@@ -612,7 +634,8 @@ def run_dist(args, rank, world, dev):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            k_, p_, _ = dist_zsort(hk.to(dev, non_blocking=True), hp.to(dev, non_blocking=True), base)
+            k_, p_, _ = dist_zsort(hk.to(dev, non_blocking=True), hp.to(dev, non_blocking=True), base,
+                                   exchange=exchange)
             rk = torch.empty(k_.shape, dtype=k_.dtype, pin_memory=True)
             rp = torch.empty(p_.shape, dtype=p_.dtype, pin_memory=True)
             rk.copy_(k_, non_blocking=True)
@@ -640,7 +663,9 @@ def run_dist(args, rank, world, dev):
             "sort_roofline": {"alg_bytes_per_key": 80, "model_ms": 1e3 * max(t_roof_hbm, t_roof_nvl),
                               "frac_of_model": 1e3 * max(t_roof_hbm, t_roof_nvl) / ms_per_step,
                               "note": "T_roof(G) = max(n/G * 80 B / HBM peak, n/G * 16 (G-1)/G B / 900 GB/s)"},
-            "exchange": {"sent_per_rank": info.get("sent"), "received_rank0": info.get("received")},
+            "exchange": {"mode": exchange, "sent_per_rank": info.get("sent"), "received_rank0": info.get("received"),
+                         "note": "p2p: the partition kernel stores into the peers' receive buffers (CUDA IPC, NVLink); "
+                                 "nccl: partition to a send buffer + all_to_all_single"},
             "gpu_launches": gpu_launches, "roofline": roof,
             "phases_ms_per_step": {k: round(v, 4) for k, v in phase_ms.items()}, "clocks": clk.summary(),
         }

@@ -212,6 +212,20 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
                            void *d_out_keys, void *d_out_payload, int64_t *h_part_counts, void *d_workspace,
                            size_t workspace_bytes, void *stream);
 
+/* Fused exchange (paper_2605_14419_b200/dist.py, exchange="p2p").  First
+ * zsb_partition_to_ranks with d_out_keys = NULL: the destination counts
+ * only (histogram + scan left in the workspace).  Then zsb_partition_send on
+ * the same workspace: the stable partition's scatter writes the records of
+ * destination d straight into d's receive buffers h_dest_keys[d] /
+ * h_dest_payload[d] (device addresses; other ranks' buffers are CUDA IPC
+ * mappings, so the stores cross NVLink) starting at h_dest_offset[d] = the
+ * records of d from lower-ranked sources -- the exchange happens inside the
+ * partition kernel, with no send buffer and no all_to_all.  Blocks until the
+ * stores are done; the caller synchronises the ranks before reading. */
+int zsb_partition_send(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, int64_t n,
+                       int32_t nparts, const uint64_t *h_dest_keys, const uint64_t *h_dest_payload,
+                       const int64_t *h_dest_offset, void *d_workspace, size_t workspace_bytes, void *stream);
+
 /* Optional per-phase device timing of zsb_sort on the calling thread (CUDA
  * events around each launch group, on the sort's own stream).  Phase slots:
  * 0 moments, 1 histogram, 2 scan, 3 scatter, 4 classify+plan, 5 finish,

@@ -39,7 +39,7 @@ EXPORTS = (
     "zsb_timing_enable", "zsb_timing_read",
     "zsb_local_moments", "zsb_bucket_histogram", "zsb_bucket_minmax", "zsb_partition_workspace_bytes",
     "zsb_partition_to_ranks", "zsb_range_histogram", "zsb_occurrence_workspace_bytes", "zsb_occurrence_index",
-    "zsb_generate", "zsb_check_violations",
+    "zsb_generate", "zsb_check_violations", "zsb_partition_send",
 )
 
 PHASES = ("moments", "histogram", "scan", "scatter", "classify", "finish", "recursion_stats", "misc")
@@ -91,6 +91,8 @@ def load(auto_build: bool = True):
     L.zsb_occurrence_index.restype = ctypes.c_int
     L.zsb_generate.argtypes = [I32, I64, I64, I64, ctypes.c_uint64, P, P, P]
     L.zsb_generate.restype = ctypes.c_int
+    L.zsb_partition_send.argtypes = [P, I32, P, I32, I64, I32, P, P, P, P, SZ, P]
+    L.zsb_partition_send.restype = ctypes.c_int
     L.zsb_check_violations.argtypes = [I32]
     L.zsb_check_violations.restype = I64
     L.zsb_bucket_histogram.argtypes = [P, I32, I64, P, I64, P, P]

@@ -63,6 +63,17 @@ struct DestCuts {
     int64_t gidx[MAX_CUTS];
 };
 
+// Fused exchange (dist.py, exchange="p2p"): the MODE_DEST scatter writes a
+// record of destination rank d straight into d's receive buffer (a CUDA IPC
+// peer pointer: NVLink stores on a multi-GPU node) at position
+// dst + delta[d], dst being its position in the local partitioned layout.
+constexpr int MAX_PEERS = MAX_CUTS + 1;
+struct PeerDest {
+    uint64_t k[MAX_PEERS];   // destination key buffers (device addresses, peers' via IPC)
+    uint64_t p[MAX_PEERS];   // destination payload buffers
+    int64_t delta[MAX_PEERS];  // this rank's chunk offset in destination d minus d's local start
+};
+
 // Per-segment partition parameters (one partition problem of the batch).
 // Level 1 is a batch of one segment covering the whole input.
 struct SegParams {
@@ -251,6 +262,8 @@ __device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p,
         return bucket_z(key_value<KK>(bits), p.center, p.std, p.zmin, p.scale, p.k);
     } else if constexpr (BM == 4) {
         return zlin();
+    } else if constexpr (BM == 5) {
+        return dest_of<KK>(bits, pos, cuts);
     } else {
         if (p.mode == MODE_ZCDF) return bucket_cdf(key_value<KK>(bits), p, cdf);
         if (p.mode == MODE_ZLIN) return zlin();

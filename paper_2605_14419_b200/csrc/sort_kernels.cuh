@@ -46,6 +46,7 @@ struct Buffers {
     const float2 *cdf;     // MODE_ZCDF only: kf knot pairs (cdf[s], cdf[s+1]) in bucket units (staged in smem)
     unsigned long long *status;  // ZSB_ERR_NAN is raised here by a finish run holding a NaN (nullable)
     int64_t n;                   // records (bounds of every buffer above; ZSB_CHECKS)
+    const PeerDest *peers;       // MODE_DEST only: write each destination's records to its (peer) buffer
 };
 
 __device__ __forceinline__ const uint64_t *src_keys(const Buffers &B, int src) {
@@ -939,9 +940,15 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 const int b = stb[i];
                 const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
                 ZSB_CHECK(b < k && (int64_t)dst >= p.start && (int64_t)dst < p.start + p.len);
-                // evict_last: the runs (and the finish's input) stay in L2
-                st_keep(dk + dst, stk[i], l2pol);
-                if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
+                if constexpr (BM == 5) {  // straight into destination b's (peer) receive buffer
+                    const int64_t at = (int64_t)dst + B.peers->delta[b];
+                    ((uint64_t *)B.peers->k[b])[at] = stk[i];
+                    if constexpr (PB != 0) ((P *)B.peers->p[b])[at] = stp[i];
+                } else {
+                    // evict_last: the runs (and the finish's input) stay in L2
+                    st_keep(dk + dst, stk[i], l2pol);
+                    if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
+                }
             }
         }
         __syncthreads();
@@ -991,8 +998,14 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             const int b = stb[i];
             const uint32_t dst = cur[b] + (uint32_t)(i - lstp[b]);
             ZSB_CHECK(b < k && (int64_t)dst >= p.start && (int64_t)dst < p.start + p.len);
-            st_keep(dk + dst, stk[i], l2pol);
-            if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
+            if constexpr (BM == 5) {
+                const int64_t at = (int64_t)dst + B.peers->delta[b];
+                ((uint64_t *)B.peers->k[b])[at] = stk[i];
+                if constexpr (PB != 0) ((P *)B.peers->p[b])[at] = stp[i];
+            } else {
+                st_keep(dk + dst, stk[i], l2pol);
+                if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
+            }
         }
     }
     SCAT_MARK(4);
@@ -1014,6 +1027,8 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
         scatter_body<KK, PB, SW, 3, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else if (!L1 && ZSB_ZLIN && mode == MODE_ZLIN)
         scatter_body<KK, PB, SW, 4, NSET>(B, segs, nseg, mat, dst_sel, prof);
+    else if (!L1 && mode == MODE_DEST && B.peers)
+        scatter_body<KK, PB, SW, 5, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else
         scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof);
 }

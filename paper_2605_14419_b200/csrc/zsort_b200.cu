@@ -412,7 +412,7 @@ int fin_prefetch(int64_t n, int pb) {
 
 template <int KK, int PB, int L1>
 int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t mat_entries, int kmax, int dst_sel,
-                     bool segs_level1 = false, cudaEvent_t after_scan = nullptr) {
+                     bool segs_level1 = false, cudaEvent_t after_scan = nullptr, int phases = 3) {
     uint32_t *mat = (uint32_t *)(c.ws + c.L.mat);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
     unsigned long long *status = (unsigned long long *)(c.ws + c.L.status);
@@ -421,6 +421,7 @@ int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t
     const size_t kbytes = hist_smem(kmax, ring);
     smem_optin(k_hist<KK, L1>, kbytes);
     const int64_t sblocks = (mat_entries + SCAN_TILE - 1) / SCAN_TILE;
+    if (phases & 1) {
     {
         PhaseScope ph(PH_HIST, c.st);
         k_hist<KK, L1><<<(unsigned)tiles, HT, kbytes, c.st>>>(c.B, segs, nseg, mat, ctrl + C_STATUS, ring ? 1 : 0, status,
@@ -433,6 +434,8 @@ int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t
     }
     ZSB_LAUNCH("k_scan");
     if (after_scan) ZSB_CUDA(cudaEventRecord(after_scan, c.st));
+    }
+    if (!(phases & 2)) return ZSB_OK;
     const size_t cdf_bytes = (c.B.cdf && segs_level1) ? (size_t)(CDF_KNOTS + 1) * 8 : 0;
     const size_t smax = (size_t)227 * 1024 - 1024;
     // 16 warps (8192-record rounds) above ZSB_SW16_ABOVE buckets: two counter
@@ -1024,6 +1027,7 @@ int injected_setup(Ctx &ctx, const void *d_keys, int32_t kd, const void *d_paylo
     ctx.B.cdf = nullptr;
     ctx.B.status = nullptr;
     ctx.B.n = n;
+    ctx.B.peers = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, k, ctx.P.tile_len, ctx.P.ntiles, 0, params[0],
@@ -1060,11 +1064,12 @@ Plan1 plan_partition(int64_t n, int pb, int nparts) {
 
 template <int KK, int PB>
 struct PartitionOp {
-    static int run(Ctx &c) {
+    static int run(Ctx &c, int phases) {
         SegParams *seg = (SegParams *)(c.ws + c.L.seg_a);
         unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
-        ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
-        return launch_partition<KK, PB>(c, seg, 1, c.P.ntiles, c.P.k * c.P.ntiles, (int)c.P.k, 2);
+        if (phases & 1) ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
+        return launch_partition_l<KK, PB, 0>(c, seg, 1, c.P.ntiles, c.P.k * c.P.ntiles, (int)c.P.k, 2, false, nullptr,
+                                             phases);
     }
 };
 
@@ -1159,6 +1164,7 @@ int sort_entry(const void *d_keys, int32_t key_dtype, const void *d_payload, int
     ctx.B.cdf = (const float2 *)(ctx.ws + ctx.L.lut);
     ctx.B.status = (unsigned long long *)(ctx.ws + ctx.L.ctrl) + C_STATUS;
     ctx.B.n = n;
+    ctx.B.peers = nullptr;
     return dispatch<SortOp>(key_dtype, payload_bytes, ctx, c, h_stats, rec);
 }
 }  // namespace
@@ -1475,7 +1481,7 @@ int zsb_range_histogram(const void *d_keys, int32_t key_dtype, int64_t n, const 
 size_t zsb_partition_workspace_bytes(int64_t n, int32_t payload_bytes, int32_t nparts) {
     if (n < 1) n = 1;
     Plan1 P = plan_partition(n, payload_bytes, nparts);
-    return make_layout(n, payload_bytes, P, false).total + align_up(sizeof(DestCuts));
+    return make_layout(n, payload_bytes, P, false).total + align_up(sizeof(DestCuts)) + align_up(sizeof(PeerDest));
 }
 
 int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes,
@@ -1494,7 +1500,7 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ctx.n = n;
     ctx.P = plan_partition(n, payload_bytes, nparts);
     ctx.L = make_layout(n, payload_bytes, ctx.P, false);
-    const size_t need = ctx.L.total + align_up(sizeof(DestCuts));
+    const size_t need = ctx.L.total + align_up(sizeof(DestCuts)) + align_up(sizeof(PeerDest));
     if (!d_workspace || workspace_bytes < need) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
     ctx.ws = (unsigned char *)d_workspace;
     ctx.st = (cudaStream_t)stream;
@@ -1523,13 +1529,14 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ctx.B.cdf = nullptr;
     ctx.B.status = nullptr;
     ctx.B.n = n;
+    ctx.B.peers = nullptr;
     SegParams *seg = (SegParams *)(ctx.ws + ctx.L.seg_a);
     int64_t *kfirst = (int64_t *)(ctx.ws + ctx.L.kfirst);
     count_launches(1);
     k_init_level1<<<1, 1, 0, ctx.st>>>(seg, kfirst, nullptr, 0, n, nparts, ctx.P.tile_len, ctx.P.ntiles, 0, 0.0, 1.0,
                                        0.0, 1.0, MODE_DEST);
     ZSB_LAUNCH("k_init_level1");
-    rc = dispatch<PartitionOp>(key_dtype, payload_bytes, ctx);
+    rc = dispatch<PartitionOp>(key_dtype, payload_bytes, ctx, d_out_keys ? 3 : 1);
     if (rc) return rc;
     // per-destination totals from the scanned matrix: starts at tile 0 of each part
     std::vector<uint32_t> starts(nparts);
@@ -1539,6 +1546,54 @@ int zsb_partition_to_ranks(const void *d_keys, int32_t key_dtype, const void *d_
     ZSB_CUDA(cudaStreamSynchronize(ctx.st));
     for (int j = 0; j < nparts; j++)
         h_part_counts[j] = (int64_t)((j + 1 < nparts) ? starts[j + 1] : (uint32_t)n) - (int64_t)starts[j];
+    return ZSB_OK;
+}
+
+
+int zsb_partition_send(const void *d_keys, int32_t key_dtype, const void *d_payload, int32_t payload_bytes, int64_t n,
+                       int32_t nparts, const uint64_t *h_dest_keys, const uint64_t *h_dest_payload,
+                       const int64_t *h_dest_offset, void *d_workspace, size_t workspace_bytes, void *stream) {
+    int rc = check_common(d_keys, key_dtype, payload_bytes, n);
+    if (rc) return rc;
+    if (nparts < 1 || nparts > MAX_PEERS || !h_dest_keys || !h_dest_offset || (payload_bytes && !h_dest_payload))
+        return fail(ZSB_ERR_ARG, "need 1 <= nparts <= 16 and destination tables");
+    if (n == 0) return ZSB_OK;
+    Ctx ctx;  // the plan and layout of the zsb_partition_to_ranks call (counts only) on this workspace
+    ctx.n = n;
+    ctx.P = plan_partition(n, payload_bytes, nparts);
+    ctx.L = make_layout(n, payload_bytes, ctx.P, false);
+    const size_t need = ctx.L.total + align_up(sizeof(DestCuts)) + align_up(sizeof(PeerDest));
+    if (!d_workspace || workspace_bytes < need) return fail(ZSB_ERR_WORKSPACE, "workspace too small");
+    ctx.ws = (unsigned char *)d_workspace;
+    ctx.st = (cudaStream_t)stream;
+    // local starts of the destinations (the scanned matrix at tile 0), then delta = offset - start
+    std::vector<uint32_t> starts(nparts);
+    const uint32_t *mat = (const uint32_t *)(ctx.ws + ctx.L.mat);
+    ZSB_CUDA(cudaMemcpy2DAsync(starts.data(), sizeof(uint32_t), mat, (size_t)ctx.P.ntiles * 4, sizeof(uint32_t),
+                               nparts, cudaMemcpyDeviceToHost, ctx.st));
+    ZSB_CUDA(cudaStreamSynchronize(ctx.st));
+    PeerDest hp{};
+    for (int j = 0; j < nparts; j++) {
+        hp.k[j] = h_dest_keys[j];
+        hp.p[j] = payload_bytes ? h_dest_payload[j] : 0;
+        hp.delta[j] = h_dest_offset[j] - (int64_t)starts[j];
+    }
+    PeerDest *pd = (PeerDest *)(ctx.ws + ctx.L.total + align_up(sizeof(DestCuts)));
+    ZSB_CUDA(cudaMemcpyAsync(pd, &hp, sizeof(hp), cudaMemcpyHostToDevice, ctx.st));
+    ctx.B.in_k = (const uint64_t *)d_keys;
+    ctx.B.in_p = d_payload;
+    ctx.B.tmp_k = nullptr;
+    ctx.B.tmp_p = nullptr;
+    ctx.B.out_k = nullptr;
+    ctx.B.out_p = nullptr;
+    ctx.B.cuts = (const DestCuts *)(ctx.ws + ctx.L.total);
+    ctx.B.cdf = nullptr;
+    ctx.B.status = nullptr;
+    ctx.B.n = n;
+    ctx.B.peers = pd;
+    rc = dispatch<PartitionOp>(key_dtype, payload_bytes, ctx, 2);
+    if (rc) return rc;
+    ZSB_CUDA(cudaStreamSynchronize(ctx.st));  // every record stored (peers read after the caller's barrier)
     return ZSB_OK;
 }
 

@@ -323,6 +323,36 @@ class DeviceOps:
                                                  ws.data_ptr(), wsb, self._stream()))
         return ok, op, [int(x) for x in counts]
 
+    def partition_plan(self, keys, payload, params: GlobalParams, gidx_base: int, cuts):
+        """Fused exchange, step 1: the destination counts of the stable
+        partition (histogram + scan, kept in the returned workspace)."""
+        n = keys.numel()
+        nparts = len(cuts) + 1
+        pb = payload.element_size() if payload is not None else 0
+        wsb = self.L.zsb_partition_workspace_bytes(n, pb, nparts)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        cb = (ctypes.c_int32 * max(1, len(cuts)))(*[c.bucket for c in cuts])
+        co = (ctypes.c_uint64 * max(1, len(cuts)))(*[c.ord for c in cuts])
+        cg = (ctypes.c_int64 * max(1, len(cuts)))(*[c.gidx for c in cuts])
+        counts = (ctypes.c_int64 * nparts)()
+        _lib.check(self.L.zsb_partition_to_ranks(keys.data_ptr(), self._kd(keys),
+                                                 payload.data_ptr() if payload is not None else None, pb, n,
+                                                 params.as_array(), params.k, int(gidx_base), len(cuts), cb, co, cg,
+                                                 None, None, counts, ws.data_ptr(), wsb, self._stream()))
+        return ws, [int(x) for x in counts]
+
+    def partition_send(self, keys, payload, ws, dest_keys, dest_payload, dest_offsets):
+        """Fused exchange, step 2: the partition's scatter stores every record
+        straight into its destination's receive buffers (peer pointers)."""
+        nparts = len(dest_keys)
+        pb = payload.element_size() if payload is not None else 0
+        dk = (ctypes.c_uint64 * nparts)(*[t.data_ptr() for t in dest_keys])
+        dp = (ctypes.c_uint64 * nparts)(*[t.data_ptr() for t in dest_payload]) if payload is not None else None
+        off = (ctypes.c_int64 * nparts)(*dest_offsets)
+        _lib.check(self.L.zsb_partition_send(keys.data_ptr(), self._kd(keys),
+                                             payload.data_ptr() if payload is not None else None, pb, keys.numel(),
+                                             nparts, dk, dp, off, ws.data_ptr(), ws.numel(), self._stream()))
+
     def local_sort(self, keys, payload):
         from .core import zsort
         k, p, _ = zsort(keys, payload)
@@ -355,12 +385,37 @@ class TorchComm:
         tdist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
                                 group=self.group)
 
+    def barrier(self):
+        if self.world > 1:
+            tdist.barrier(group=self.group)
+
+    def share_cuda(self, tensors):
+        """Every rank's `tensors` as device tensors usable here: this rank's own,
+        the others' opened through CUDA IPC (torch's tensor reductions: the
+        allocation's IPC handle plus offset; peer access over NVLink between
+        GPUs of a node, plain device memory between processes of one GPU)."""
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        mine = [reduce_tensor(t) for t in tensors]
+        objs = [None] * self.world
+        tdist.all_gather_object(objs, mine, group=self.group)
+        out = []
+        for r, o in enumerate(objs):
+            out.append(list(tensors) if r == self.rank else [fn(*args) for fn, args in o])
+        return out
+
 
 # ------------------------------------------------------------- the sort
 
 def dist_zsort(keys: torch.Tensor, payload: torch.Tensor | None, gidx_base: int, group=None, ops=None,
-               k: int = DEFAULT_K, comm=None):
+               k: int = DEFAULT_K, comm=None, exchange: str = "nccl"):
     """Globally stable sort of sharded records; returns this rank's slice.
+
+    exchange: "nccl" -- stable partition into a send buffer, then
+    all_to_all_single of keys and payload; "p2p" -- the fused exchange: the
+    partition's scatter stores every record straight into its destination
+    rank's receive buffer through CUDA IPC peer pointers (one kernel, no send
+    buffer, no all_to_all; needs peer access between the ranks' GPUs).
 
     keys/payload: this rank's shard (contiguous global positions starting at
     gidx_base).  Returns (keys, payload, info) where concatenating every
@@ -397,24 +452,48 @@ def dist_zsort(keys: torch.Tensor, payload: torch.Tensor | None, gidx_base: int,
     cuts = plan_cuts_exact(counts, world, rank, keys, params, gidx_base, ops, comm, kind)
     info["cuts"] = cuts
 
-    # ---- D3: stable partition by destination, all_to_all of keys and payload
-    pk, pp, send = ops.partition(keys, payload, params, gidx_base, cuts)
-    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
-    recv_t = torch.empty_like(send_t)
-    comm.all_to_all_single(recv_t, send_t)
-    recv = [int(x) for x in recv_t.tolist()]
-    rk = torch.empty(sum(recv), dtype=keys.dtype, device=dev)
-    comm.all_to_all_single(rk, pk, recv, send)
-    rp = None
-    if payload is not None:
-        rp = torch.empty(sum(recv), dtype=payload.dtype, device=dev)
-        comm.all_to_all_single(rp, pp, recv, send)
-    info.update(sent=send, received=recv)
+    # ---- D3: stable partition by destination and the exchange
+    if exchange == "p2p":
+        rk, rp, send, recv = _exchange_p2p(keys, payload, params, gidx_base, cuts, ops, comm, world, rank, dev)
+    else:
+        pk, pp, send = ops.partition(keys, payload, params, gidx_base, cuts)
+        send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+        recv_t = torch.empty_like(send_t)
+        comm.all_to_all_single(recv_t, send_t)
+        recv = [int(x) for x in recv_t.tolist()]
+        rk = torch.empty(sum(recv), dtype=keys.dtype, device=dev)
+        comm.all_to_all_single(rk, pk, recv, send)
+        rp = None
+        if payload is not None:
+            rp = torch.empty(sum(recv), dtype=payload.dtype, device=dev)
+            comm.all_to_all_single(rp, pp, recv, send)
+    info.update(sent=send, received=recv, exchange=exchange)
     # ---- local stable sort of the received records (global input order)
     if rk.numel() == 0:
         return rk, rp, info
     ok, op = ops.local_sort(rk, rp)
     return ok, op, info
+
+
+def _exchange_p2p(keys, payload, params, gidx_base, cuts, ops, comm, world, rank, dev):
+    """Fused partition + exchange: counts (all_gather), receive buffers shared
+    by IPC, then one scatter kernel writes every record into its destination
+    rank's buffer at (records of that destination from lower-ranked sources)
+    + its stable position.  Chunks land in source-rank order, as all_to_all
+    delivers them."""
+    ws, send = ops.partition_plan(keys, payload, params, gidx_base, cuts)
+    allc = torch.stack(comm.all_gather(torch.tensor(send, dtype=torch.int64, device=dev))).cpu().numpy()  # (src, dst)
+    recv = [int(x) for x in allc[:, rank]]
+    rk = torch.empty(sum(recv), dtype=keys.dtype, device=dev)
+    rp = torch.empty(sum(recv), dtype=payload.dtype, device=dev) if payload is not None else None
+    shared = comm.share_cuda([rk] + ([rp] if rp is not None else []))  # per rank: [keys buf, payload buf]
+    offsets = [int(allc[:rank, d].sum()) for d in range(world)]
+    ops.partition_send(keys, payload, ws, [shared[d][0] for d in range(world)],
+                       [shared[d][1] for d in range(world)] if payload is not None else None, offsets)
+    comm.barrier()  # every rank's stores into this rank's buffers are done
+    del shared
+    comm.barrier()  # the peers' mappings are released before the buffers can be freed
+    return rk, rp, send, recv
 
 
 def _ord_to_bits(o: int, kind: str) -> int:

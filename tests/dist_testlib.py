@@ -47,6 +47,12 @@ class ThreadComm:
     def all_gather(self, t):
         return [v.to(t.device) for v in self._exchange(t.clone())]
 
+    def barrier(self):
+        self.g.barrier.wait()
+
+    def share_cuda(self, tensors):
+        return self._exchange(list(tensors))  # one process: every rank's buffers are plain device memory
+
     def all_to_all_single(self, out, inp, out_splits=None, in_splits=None):
         if in_splits is None:
             in_splits = [inp.numel() // self.world] * self.world
@@ -136,7 +142,7 @@ class NumpyOps:
         return torch.from_numpy(np.ascontiguousarray(k)), (torch.from_numpy(np.ascontiguousarray(p)) if p is not None else None)
 
 
-def run_threads(shards, ops_factory, k=1024):
+def run_threads(shards, ops_factory, k=1024, exchange="nccl"):
     """Run dist_zsort on len(shards) simulated ranks; returns per-rank outputs."""
     from paper_2605_14419_b200.dist import dist_zsort
 
@@ -152,7 +158,8 @@ def run_threads(shards, ops_factory, k=1024):
             ops = ops_factory()
             if hasattr(ops.device, "type") and ops.device.type == "cuda":
                 torch.cuda.set_device(ops.device)
-            results[r] = dist_zsort(keys, pay, int(bases[r]), ops=ops, comm=ThreadComm(grp, r), k=k)
+            results[r] = dist_zsort(keys, pay, int(bases[r]), ops=ops, comm=ThreadComm(grp, r), k=k,
+                                    exchange=exchange)
         except BaseException as exc:  # surface in the main thread
             errors.append(exc)
             grp.barrier.abort()
@@ -215,8 +222,14 @@ class StagedComm:
         self.inner.all_to_all_single(h, inp.cpu(), out_splits, in_splits)
         out.copy_(h)
 
+    def barrier(self):
+        self.inner.barrier()
 
-def gloo_device_worker(rank, world, port, keys_all, pay_all, out_dir, k):
+    def share_cuda(self, tensors):
+        return self.inner.share_cuda(tensors)
+
+
+def gloo_device_worker(rank, world, port, keys_all, pay_all, out_dir, k, exchange="nccl"):
     """torch.multiprocessing target: one process per rank on cuda:0 running
     dist_zsort with the product DeviceOps (CUDA kernels through the C ABI)
     and TorchComm over gloo (staged through host memory)."""
@@ -234,7 +247,7 @@ def gloo_device_worker(rank, world, port, keys_all, pay_all, out_dir, k):
         lo, hi = rank * n // world, (rank + 1) * n // world
         keys = torch.from_numpy(np.ascontiguousarray(keys_all[lo:hi])).to(dev)
         pay = torch.from_numpy(np.ascontiguousarray(pay_all[lo:hi])).to(dev)
-        ok, op, info = dist_zsort(keys, pay, lo, ops=DeviceOps(dev), comm=StagedComm(), k=k)
+        ok, op, info = dist_zsort(keys, pay, lo, ops=DeviceOps(dev), comm=StagedComm(), k=k, exchange=exchange)
         np.save(os.path.join(out_dir, f"k{rank}.npy"), ok.cpu().numpy())
         np.save(os.path.join(out_dir, f"p{rank}.npy"), op.cpu().numpy())
     finally:

@@ -122,6 +122,50 @@ def test_simulated_ranks_gpu(world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_simulated_ranks_gpu_fused_exchange(world):
+    """exchange="p2p": the partition kernel stores every record into its
+    destination rank's buffer (here the ranks are threads of one process, so
+    the peer pointers are plain device pointers)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_14419_b200.dist import DeviceOps
+
+    dev = torch.device("cuda", 0)
+    for name, keys in datasets():
+        outs = run_threads(shards_of(keys, world, dev), lambda: DeviceOps(dev), k=1024, exchange="p2p")
+        check(keys, outs)
+    keys = config5_small(1 << 21)
+    outs = run_threads(shards_of(keys, world, dev), lambda: DeviceOps(dev), k=4096, exchange="p2p")
+    sizes = [o[0].numel() for o in outs]
+    assert max(sizes) - min(sizes) <= 1, sizes
+    check(keys, outs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["config5_recipe", "heavy_run", "signed_zeros"])
+def test_two_processes_fused_exchange_ipc(name):
+    """The fused exchange across real processes: each rank's receive
+    buffers are opened by the other through CUDA IPC and the partition kernel
+    stores straight into them (on one GPU here; across GPUs the same stores
+    travel over NVLink)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    keys = dict(datasets())[name]
+    if name == "config5_recipe":
+        keys = config5_small(1 << 20)
+    pay = np.arange(keys.size, dtype=np.int64)
+    with tempfile.TemporaryDirectory() as td:
+        mp.start_processes(gloo_device_worker, args=(2, _free_port(), keys, pay, td, 4096, "p2p"), nprocs=2,
+                           join=True, start_method="spawn")
+        outs = [(torch.from_numpy(np.load(f"{td}/k{r}.npy")), torch.from_numpy(np.load(f"{td}/p{r}.npy")))
+                for r in range(2)]
+    check(keys, outs)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", ["config5_recipe", "normal_f64", "heavy_run", "signed_zeros"])
 def test_two_processes_device_ops_gloo(name):
     """The product distributed path in real processes: two ranks on cuda:0,

@@ -22,6 +22,7 @@ from tests.dist_testlib import run_threads  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--world", type=int, default=4)
 ap.add_argument("--log2n", type=int, default=26, help="records per rank = 2^log2n")
+ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"])
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 per = 1 << a.log2n
@@ -29,10 +30,10 @@ n = per * a.world
 keys = datagen.config5_keys(0, n, 1 << 31, device="cuda")
 shards = [(keys[r * per:(r + 1) * per], torch.arange(r * per, (r + 1) * per, dtype=torch.int64, device=dev))
           for r in range(a.world)]
-run_threads(shards, lambda: DeviceOps(dev), k=4096)  # warm-up
+run_threads(shards, lambda: DeviceOps(dev), k=4096, exchange=a.exchange)  # warm-up
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-outs = run_threads(shards, lambda: DeviceOps(dev), k=4096)
+outs = run_threads(shards, lambda: DeviceOps(dev), k=4096, exchange=a.exchange)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 ok = torch.cat([o[0] for o in outs])
