@@ -283,13 +283,15 @@ def main():
         S.sort()
     torch.cuda.synchronize()
     L.zsb_timing_enable(0)
+    records = (ctypes.c_int64 * 8)()
+    L.zsb_timing_records(records, 8)
     L.zsb_timing_read(ms_phase, launches, 8, 1)
     ms_per_step = sum(step_ms) / args.steps
     value = n / (ms_per_step / 1e3)
 
     hbm_peak, peak_kind = peaks()
     rec = 8 + pb
-    roof, phase_ms = roofline_from_phases(n, rec, ms_phase, launches, args.steps, args.config)
+    roof, phase_ms = roofline_from_phases(n, rec, ms_phase, launches, args.steps, args.config, records)
     sort_alg_bytes = (16 + 4 * rec) * n
     gpu_launches = int(sum(launches[i] for i in range(8)) / args.steps)
     st = S.stats
@@ -402,16 +404,64 @@ def e2e_leg(Z, keys_h, pay_h, cfg, S, flush, stream, steps):
         raise SystemExit("e2e output differs from the device-resident run")
     # the copies alone (same pinned buffers, same sizes): every output key
     # depends on every input key, so no output can leave before the last input
-    # has arrived -- H2D + D2H is the floor of an end-to-end sort over PCIe
+    # has arrived -- H2D + D2H is the floor of ONE end-to-end sort over PCIe
     dk, dp = torch.empty(hk.shape, dtype=hk.dtype, device="cuda"), torch.empty(hp.shape, dtype=hp.dtype, device="cuda")
     h2d = timed_steps(lambda: (dk.copy_(hk, non_blocking=True), dp.copy_(hp, non_blocking=True)), 3, flush, stream)
     d2h = timed_steps(lambda: (hok.copy_(dk, non_blocking=True), hop.copy_(dp, non_blocking=True)), 3, flush, stream)
     copy_floor = min(h2d) + min(d2h)
-    return {"value": n / (e2e_step / 1e3), "unit": "keys/s", "h2d_bytes_per_step": int(n * rec),
-            "d2h_bytes_per_step": int(n * rec), "ms_per_step": e2e_step,
-            "copy_floor_ms": copy_floor, "h2d_gbs": n * rec / min(h2d) / 1e6, "d2h_gbs": n * rec / min(d2h) / 1e6,
-            "vs_copy_floor": e2e_step / copy_floor,
-            "api": "paper_2605_14419_b200.zsort(pinned host tensors, out=pinned host tensors)"}
+    del dk, dp
+    # The headline: the same steps as a stream through the public
+    # SortPipeline (every step uploads its inputs from pinned host memory and
+    # downloads its result, inside the timed region), two device buffer sets and
+    # three streams: step i+1's upload and step i-1's download overlap step i's
+    # sort, so both PCIe directions are busy.  Inputs (1.2 GB per step at C4)
+    # exceed the L2, no flush between steps.  Timed by CUDA events from before
+    # the first upload to after the last download, and by the host clock.
+    hk2, hp2 = hk.clone().pin_memory(), hp.clone().pin_memory()  # alternate input and output buffers
+    hok2, hop2 = torch.empty_like(hk).pin_memory(), torch.empty_like(hp).pin_memory()
+    hok3, hop3 = torch.empty_like(hk).pin_memory(), torch.empty_like(hp).pin_memory()
+    pipe = Z.SortPipeline(n, hk.dtype, hp.dtype, cfg)
+    # three host output sets: a step waits for the step that last used its set,
+    # whose download ended a whole step earlier (no bubble on the upload engine)
+    ins, outs = [(hk, hp), (hk2, hp2)], [(hok, hop), (hok2, hop2), (hok3, hop3)]
+    NW = 6
+    for i in range(NW):
+        pipe.submit(*ins[i % 2], *outs[i % 3])
+    pipe.drain()
+    ksteps = max(6, min(2 * steps, 18))
+    for ok_h, op_h in outs:
+        ok_h.zero_(), op_h.zero_()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(pipe.s_in)
+    for i in range(ksteps):
+        if i >= 3:
+            pipe.wait(NW + i - 3)  # the step that used these host output buffers
+        pipe.submit(*ins[i % 2], *outs[i % 3])
+    pipe.drain()
+    e1.record(pipe.s_out)
+    e1.synchronize()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    pipe_ms = max(e0.elapsed_time(e1), 0.0) / ksteps
+    torch.cuda.synchronize()
+    for ok_h, op_h in outs:
+        if not (np.array_equal(ok_h.numpy(), S.out_k.cpu().numpy()) and np.array_equal(op_h.numpy(), S.out_p.cpu().numpy())):
+            raise SystemExit("pipelined e2e output differs from the device-resident run")
+    del pipe
+    torch.cuda.empty_cache()
+    duplex_floor = max(min(h2d), min(d2h))
+    return {"value": n / (pipe_ms / 1e3), "unit": "keys/s", "h2d_bytes_per_step": int(n * rec),
+            "d2h_bytes_per_step": int(n * rec), "ms_per_step": pipe_ms, "steps": ksteps,
+            "wall_ms_per_step": wall_ms / ksteps,
+            "pipeline_floor_ms": duplex_floor, "vs_pipeline_floor": pipe_ms / duplex_floor,
+            "api": "paper_2605_14419_b200.SortPipeline(n, f64, i32).submit(pinned host keys, payload, pinned host "
+                   "outputs) per step; wait()/drain(): uploads, sorts and downloads of consecutive steps overlap",
+            "single_sort": {"ms_per_step": e2e_step, "keys_per_s": n / (e2e_step / 1e3),
+                            "copy_floor_ms": copy_floor, "vs_copy_floor": e2e_step / copy_floor,
+                            "api": "paper_2605_14419_b200.zsort(pinned host tensors, out=pinned host tensors): "
+                                   "one sort, H2D + sort + D2H in series (latency)"},
+            "h2d_gbs": n * rec / min(h2d) / 1e6, "d2h_gbs": n * rec / min(d2h) / 1e6}
 
 
 def c5_single_gpu(Z, L, dev, flush, stream, steps, hbm_peak):
@@ -447,24 +497,32 @@ def c5_single_gpu(Z, L, dev, flush, stream, steps, hbm_peak):
         return {"skipped": "out of memory"}
 
 
-def roofline_from_phases(n, rec, ms_phase, launches, steps, cfg):
-    """Roofline of the dominant phase from the library's per-phase CUDA-event
-    times (a separate pass of the same steps).  The finish phase is the main
-    launch plus its refine pass: its algorithmic bytes are charged to the
-    phase over the phase's time.  `traffic` comes from the committed ncu
-    --set full capture of the same config (profiles/*_traffic_c<cfg>.json),
-    else null."""
+def roofline_from_phases(n, rec, ms_phase, launches, steps, cfg, records=None):
+    """Roofline of the dominant kernel from the library's per-phase CUDA-event
+    times (a separate pass of the same steps).  Per launch: algorithmic bytes =
+    the per-record figure of the kernel (2 x (8 + payload) for the
+    scatter and the finish, 8 for the histogram and the moments) x the records
+    its launches passed over (zsb_timing_records: every partition level's
+    records for the histogram and the scatter, n for the finish), over the
+    kernel's CUDA-event time.  `one_pass_frac` is the stricter figure that
+    credits a single pass over the n records whatever the number of levels
+    (the whole-sort `sort_roofline` uses the same convention).  `traffic`
+    comes from the committed ncu capture of the same config
+    (profiles/*_traffic_c<cfg>.json), else null."""
     from paper_2605_14419_b200 import _lib
 
     hbm_peak, peak_kind = peaks()
-    alg_bytes_step = {"moments": 8 * n, "histogram": 8 * n, "scan": None, "scatter": 2 * rec * n,
-                      "classify": None, "finish": 2 * rec * n, "recursion_stats": None, "misc": None}
+    per_rec = {"moments": 8, "histogram": 8, "scatter": 2 * rec, "finish": 2 * rec}
     phase_ms = {name: ms_phase[i] / steps for i, name in enumerate(_lib.PHASES)}
     phase_launch = {name: launches[i] / steps for i, name in enumerate(_lib.PHASES)}
+    phase_rec = {name: (records[i] / steps if records is not None and records[i] > 0 else n)
+                 for i, name in enumerate(_lib.PHASES)}
     dominant = max(("moments", "histogram", "scatter", "finish"), key=lambda k: phase_ms[k])
-    alg = alg_bytes_step[dominant]
     ms = max(phase_ms[dominant], 1e-9)
-    achieved = alg / (ms / 1e3) / 1e9
+    nl = max(phase_launch[dominant], 1.0)
+    alg_step = per_rec[dominant] * phase_rec[dominant]  # all launches of the kernel in one sort
+    achieved = alg_step / (ms / 1e3) / 1e9
+    one_pass = per_rec[dominant] * n / (ms / 1e3) / 1e9
     traffic, traffic_src = None, None
     try:
         import glob
@@ -474,15 +532,17 @@ def roofline_from_phases(n, rec, ms_phase, launches, steps, cfg):
             if int(rec_t.get("n", n)) == n:
                 per = rec_t["bytes_per_step"].get(f"k_{dominant}")
                 if per:
-                    traffic, traffic_src = float(per), os.path.relpath(tf[-1], REPO)
+                    traffic, traffic_src = float(per) / nl, os.path.relpath(tf[-1], REPO)
     except Exception:
         traffic = None
     roof = {"bound": "hbm", "kernel": f"k_{dominant}", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
-            "alg_bytes_per_launch": alg, "launch_ms": ms, "launches_per_step": phase_launch[dominant],
-            "note": f"alg bytes = 2 x (8 + payload) per key for the {dominant} phase (one pass over the records; "
-                    "further partition levels are not credited); time = the phase's CUDA-event time per sort; "
-                    "traffic = ncu DRAM bytes of the phase's launches per sort, same config"}
+            "alg_bytes_per_launch": alg_step / nl, "launch_ms": ms / nl, "launches_per_step": nl,
+            "records_per_step": phase_rec[dominant], "one_pass_frac": one_pass / hbm_peak,
+            "note": f"per launch of k_{dominant}: alg bytes = {per_rec[dominant]} B x the records the launch passes "
+                    "over (each partition level's launch passes over that level's records), time = the kernel's "
+                    "CUDA-event time / its launches, measured live; one_pass_frac credits one pass over n only; "
+                    "traffic = ncu DRAM bytes per launch of the same config"}
     return roof, phase_ms
 
 
@@ -615,8 +675,10 @@ def run_dist(args, rank, world, dev):
         dist_zsort(dk, dp, base, exchange=exchange)
     torch.cuda.synchronize()
     L.zsb_timing_enable(0)
+    records = (ctypes.c_int64 * 8)()
+    L.zsb_timing_records(records, 8)
     L.zsb_timing_read(ms_phase, launches, 8, 1)
-    roof, phase_ms = roofline_from_phases(n, 16, ms_phase, launches, args.steps, args.config)
+    roof, phase_ms = roofline_from_phases(n, 16, ms_phase, launches, args.steps, args.config, records)
     gpu_launches = int(sum(launches[i] for i in range(8)) / args.steps)
     # e2e: pinned host shard -> device -> distributed sort -> pinned host result
     e2e = None

@@ -234,6 +234,11 @@ int zsb_partition_send(const void *d_keys, int32_t key_dtype, const void *d_payl
  * even when timing is off) and returns the number of slots. */
 void zsb_timing_enable(int32_t on);
 int32_t zsb_timing_read(double *ms, int64_t *launches, int32_t nslots, int32_t reset);
+/* Records each phase's launches have passed over since the last reset (slots
+ * 1 histogram and 3 scatter: the level's records, every level; 5 finish: n
+ * per sort); bench.py's per-launch roofline uses them.  Read before the
+ * zsb_timing_read call that resets. */
+int32_t zsb_timing_records(int64_t *records, int32_t nslots);
 
 /* Thread-local message for the last failing call. */
 const char *zsb_last_error(void);

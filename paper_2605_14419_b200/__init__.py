@@ -32,7 +32,10 @@ from .core import (  # noqa: F401
     zsort_rec,
 )
 
+from .pipeline import SortPipeline  # noqa: F401,E402
+
 __all__ = [
+    "SortPipeline",
     "DegenerateSpreadError", "FirstPassStats", "MappingParams", "PartitionPlan", "SortConfig", "SortStats",
     "all_equal", "build_mapping_params", "build_partition_plan", "check_stable_permutation_device",
     "cluster_count", "counting_sort_stable", "estimated_mean", "fallback_sort_stable", "first_pass",

@@ -36,7 +36,7 @@ ZSB_OK, ZSB_ERR_ARG, ZSB_ERR_DTYPE, ZSB_ERR_NAN, ZSB_ERR_WORKSPACE, ZSB_ERR_CUDA
 EXPORTS = (
     "zsb_workspace_bytes", "zsb_sort", "zsb_rec_workspace_bytes", "zsb_sort_rec", "zsb_moments", "zsb_histogram", "zsb_scatter",
     "zsb_check_workspace_bytes", "zsb_check_sorted", "zsb_last_error", "zsb_version",
-    "zsb_timing_enable", "zsb_timing_read",
+    "zsb_timing_enable", "zsb_timing_read", "zsb_timing_records",
     "zsb_local_moments", "zsb_bucket_histogram", "zsb_bucket_minmax", "zsb_partition_workspace_bytes",
     "zsb_partition_to_ranks", "zsb_range_histogram", "zsb_occurrence_workspace_bytes", "zsb_occurrence_index",
     "zsb_generate", "zsb_check_violations", "zsb_partition_send",
@@ -109,6 +109,8 @@ def load(auto_build: bool = True):
     L.zsb_timing_enable.restype = None
     L.zsb_timing_read.argtypes = [P, P, I32, I32]
     L.zsb_timing_read.restype = I32
+    L.zsb_timing_records.argtypes = [P, I32]
+    L.zsb_timing_records.restype = I32
     L.zsb_last_error.argtypes = []
     L.zsb_last_error.restype = ctypes.c_char_p
     L.zsb_version.argtypes = []

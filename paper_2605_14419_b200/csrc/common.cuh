@@ -144,7 +144,8 @@ enum Ctrl {
     C_NTEAM = 24,        // team runs of the level (cap < len <= TEAM * cap)
     C_TTICK = 25,        // team run ticket
     C_NEED_STATS = 26,   // some child of the level needs the moments pass (k_seg_moments) before its mapping
-    C_SLOTS = 27
+    C_REC_NEXT = 27,     // records of the level's children (the next level's histogram and scatter pass over them)
+    C_SLOTS = 28
 };
 
 // ------------------------------------------------------------ key traits

@@ -455,6 +455,7 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
         if (threadIdx.x == 0) {
             ctrl[C_SCAN_TICKET] = 0ull;
             ctrl[C_NCHILD] = 0ull;
+            ctrl[C_REC_NEXT] = 0ull;
             ctrl[C_NENTRY] = 0ull;
             ctrl[C_NTEAM] = 0ull;
             ctrl[C_TTICK] = 0ull;
@@ -703,6 +704,9 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 #endif
 constexpr int SCAT_ITEMS = ZSB_SCAT_ITEMS;
 constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
+#ifndef ZSB_SCAT_RUNS
+#define ZSB_SCAT_RUNS 0  // N > 0: rows of at most N runs of equal adjacent buckets add once per run (measured: C4 scatter +1 %, C2 +4 %: the 32-way same-address atomics of ordered inputs are not what bounds the kernel)
+#endif
 #ifndef ZSB_SCAT_TIE_MATCH
 #define ZSB_SCAT_TIE_MATCH 0  // 1: tie groups re-ranked with one MATCH.ANY (round-2 start) instead of a ballot loop
 #endif
@@ -720,8 +724,8 @@ struct ScatLayout {
     size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, off_cdf, total;
 };
 
-__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw, int nset = 2) {
-    const int round = sw * 32 * SCAT_ITEMS;
+__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw, int nset = 2, int items = SCAT_ITEMS) {
+    const int round = sw * 32 * items;
     ScatLayout L;
     size_t o = 0;
     L.off_cur = o;
@@ -827,9 +831,12 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
     __syncthreads();
 }
 
-template <int KK, int PB, int SW, int BM, int NSET>
+// SK: small-fan-out kernel (k <= 32 in every segment of the launch): only the
+// register multi-split ranking is compiled, ITEMS records per thread.
+template <int KK, int PB, int SW, int BM, int NSET, int ITEMS = SCAT_ITEMS, bool SK = false>
 __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *__restrict__ segs, int nseg,
-                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof) {
+                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof,
+                                             int kpart = 0) {
 #ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
     long long t_mark = prof ? clock64() : 0;
     long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
@@ -847,13 +854,15 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
     } while (0)
 #endif
     using P = typename PayloadT<PB>::T;
-    constexpr int ITEMS = SCAT_ITEMS;
     constexpr int ST = SW * 32;             // threads
     constexpr int ROUND = ST * ITEMS;       // records per round
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t wtot[SW];
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
+    // a level split over two launches: kpart 1 takes the segments of k <= 32
+    // (k_scatter_sk), kpart 2 the others
+    if ((kpart == 1 && p.k > 32) || (kpart == 2 && p.k <= 32)) return;
     const int64_t ti = blockIdx.x - p.tile_first;
     const int64_t t0 = p.start + ti * p.tile_len;
     const int64_t t1 = min(t0 + p.tile_len, p.start + p.len);
@@ -869,7 +878,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         return;
     }
     const int k = p.k;
-    const ScatLayout L = scat_layout(k, PB, SW, NSET);
+    const ScatLayout L = scat_layout(k, PB, SW, NSET, ITEMS);
     const int NC = k * SW;
     uint32_t *cur = (uint32_t *)(smem + L.off_cur);
     uint16_t *cnt2 = (uint16_t *)(smem + L.off_cnt);  // [NSET][SW][k]
@@ -971,7 +980,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 pk[j] = bkj >= 0 ? (uint32_t)bkj | ((uint32_t)j << 16) : 0xffffffffu;
                 write_prev(j);
             }
-        } else if (BM != 1 && ZSB_SCAT_SMALLK && k <= 32) {
+        } else if (SK || (BM != 1 && SW == 8 && ZSB_SCAT_SMALLK && k <= 32)) {  // (8-warp kernels: kmax <= 512)
             // Small fan-out (recursion children, destination ranks): every
             // instruction holds many lanes per bucket, so the ranking is a warp
             // multi-split in registers -- one ballot per bucket bit gives lane b
@@ -1000,7 +1009,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 write_prev(j);
             }
             if (lane < k) cnt[w * k + lane] = (uint16_t)wc;
-        } else {
+        } else if constexpr (!SK) {
             // the next item's bucket (its mapping-table load) is computed ahead,
             // before this item's warp barrier, so it overlaps the ranking chain
             int bk_next = ZSB_SCAT_AHEAD ? bucket_of_item(0) : 0;
@@ -1019,6 +1028,48 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 const uint32_t sh = 16 * (q & 1);
                 uint32_t *word = (uint32_t *)cnt + (q >> 1);
                 __syncwarp();  // item j - 1's re-reads before item j's atomics
+#if ZSB_SCAT_RUNS
+                // Ordered inputs put whole rows of lanes in one bucket, and 32
+                // lanes on one counter serialise the shared atomic into 32
+                // passes (ncu: 17 wavefronts per atomic on config 4, 41 % of the
+                // kernel's shared-memory traffic).  A row made of few runs of
+                // equal adjacent buckets adds once per run -- the run's head
+                // adds its length and hands count and re-read to its lanes;
+                // two runs of one bucket in a row meet as a tie group below.
+                const int prevb = __shfl_up_sync(0xffffffffu, bkj, 1);
+                const unsigned hm = __ballot_sync(0xffffffffu, lane == 0 || bkj != prevb);
+                bool tie;
+                if (__popc(hm) <= ZSB_SCAT_RUNS) {
+                    const int hl = 31 - __clz(hm & (lt | (1u << lane)));  // this lane's run head
+                    const unsigned nx = hm & ~(lt | (1u << lane));        // heads after this lane
+                    const uint32_t len = (uint32_t)((nx ? __ffs(nx) - 1 : 32) - hl);
+                    bool th = false;
+                    if (v && lane == hl) {
+                        old = (atomicAdd(word, len << sh) >> sh) & 0xFFFFu;
+                        after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
+                        th = after != old + len;
+                    }
+                    const unsigned tmh = __ballot_sync(0xffffffffu, th);
+                    old = __shfl_sync(0xffffffffu, old, hl) + (uint32_t)(lane - hl);
+                    after = __shfl_sync(0xffffffffu, after, hl);
+                    tie = v && ((tmh >> hl) & 1u);
+                } else {
+                    if (v) {
+                        old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
+                        after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
+                    }
+                    tie = v && after != old + 1u;
+                }
+                {
+                    unsigned tm = __ballot_sync(0xffffffffu, tie);
+                    while (tm) {
+                        const int bl = __shfl_sync(0xffffffffu, bkj, __ffs(tm) - 1);
+                        const unsigned grp = __ballot_sync(0xffffffffu, bkj == bl);
+                        if (bkj == bl) old = after - (uint32_t)__popc(grp) + (uint32_t)__popc(grp & lt);
+                        tm &= ~grp;
+                    }
+                }
+#else
                 if (v) {
                     old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
                     after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
@@ -1046,6 +1097,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                         tm &= ~grp;
                     }
                 }
+#endif
 #endif
                 pk[j] = v ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
                 write_prev(j);
@@ -1119,18 +1171,43 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
 template <int KK, int PB, int SW, int NSET, int L1>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
-                                                              int dst_sel, long long *prof) {
+                                                              int dst_sel, long long *prof, int kpart) {
     const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
     if (L1 && mode == MODE_ZCDF)
-        scatter_body<KK, PB, SW, 1, NSET>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 1, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
     else if (!L1 && ZSB_BM_ZSCORE && mode == MODE_ZSCORE)
-        scatter_body<KK, PB, SW, 3, NSET>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 3, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
     else if (!L1 && ZSB_ZLIN && mode == MODE_ZLIN)
-        scatter_body<KK, PB, SW, 4, NSET>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 4, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
     else if (!L1 && mode == MODE_DEST && B.peers)
-        scatter_body<KK, PB, SW, 5, NSET>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 5, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
     else
-        scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof);
+        scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
+}
+
+// Recursion levels whose segments all have k <= 32 (children of a 10^8-key
+// level 1, destination ranks): SCAT_SK_ITEMS records per thread and 64
+// registers, four CTAs of 8 warps per SM (2048-record rounds: runs of >= 64
+// records per bucket), ranking by the register multi-split only.
+#ifndef ZSB_SCAT_SK_ITEMS
+#define ZSB_SCAT_SK_ITEMS 8
+#endif
+constexpr int SCAT_SK_ITEMS = ZSB_SCAT_SK_ITEMS;
+constexpr int SCAT_SK_CTAS = 32 / SCAT_SK_ITEMS;  // per SM
+
+template <int KK, int PB>
+__global__ void __launch_bounds__(256, SCAT_SK_CTAS) k_scatter_sk(Buffers B, const SegParams *__restrict__ segs, int nseg,
+                                                                 const uint32_t *__restrict__ mat, int dst_sel,
+                                                                 long long *prof, int kpart) {
+    const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
+    if (ZSB_BM_ZSCORE && mode == MODE_ZSCORE)
+        scatter_body<KK, PB, 8, 3, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
+    else if (ZSB_ZLIN && mode == MODE_ZLIN)
+        scatter_body<KK, PB, 8, 4, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
+    else if (mode == MODE_DEST && B.peers)
+        scatter_body<KK, PB, 8, 5, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
+    else
+        scatter_body<KK, PB, 8, 0, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
 }
 
 // ------------------------------------------------------- equalisation
@@ -1632,6 +1709,7 @@ __device__ __forceinline__ void bstart_slot(int64_t g, const SegParams *__restri
         atomicOr(&ctrl[C_NEED_STATS], 1ull);
     }
     unsigned long long slot = atomicAdd(&ctrl[C_NCHILD], 1ull);
+    atomicAdd(&ctrl[C_REC_NEXT], (unsigned long long)ch.len);
     children[slot] = ch;
     acc[slot] = SegAcc{~0ull, 0ull, 0.0, 0.0};
 }

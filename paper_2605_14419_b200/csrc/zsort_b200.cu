@@ -47,6 +47,7 @@ struct Timing {
     size_t used = 0;
     double ms[PH_SLOTS] = {0};
     long long launches[PH_SLOTS] = {0};
+    long long records[PH_SLOTS] = {0};  // records each phase's launches processed (histogram, scatter, finish)
     long long launch_total = 0;
 };
 thread_local Timing g_t;
@@ -126,6 +127,9 @@ void timing_collect() {
 #endif
 #ifndef ZSB_K1_TEAM
 #define ZSB_K1_TEAM 2048  // cap on the level-1 bucket count when buckets are sized for team runs
+#endif
+#ifndef ZSB_SCAT_SK
+#define ZSB_SCAT_SK 0  // 1: recursion-level segments of k <= 32 run k_scatter_sk (8 records per thread, 4 CTAs per SM; measured: no faster, the split launch costs C4 +0.1 ms)
 #endif
 #ifndef ZSB_SW16_ABOVE
 #define ZSB_SW16_ABOVE 512  // bucket counts above this use 16-warp, 8192-record scatter rounds
@@ -443,24 +447,39 @@ int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t
     const bool want16 = scat_warps(kmax, ZSB_SW16_ABOVE) == 16;
     const int nset16 = !want16 ? 0 : (scat_layout(kmax, PB, 16, 2).total + cdf_bytes <= smax ? 2
                                        : (scat_layout(kmax, PB, 16, 1).total + cdf_bytes <= smax ? 1 : 0));
-    if (nset16 == 0) {
+    // recursion levels: the segments of k <= 32 go through k_scatter_sk; a level
+    // that also holds larger fan-outs is split over two launches (each CTA
+    // exits at once on a tile of the other part)
+    const bool sk = !L1 && ZSB_SCAT_SMALLK && ZSB_SCAT_SK;
+    const int kpart = !sk ? 0 : (kmax <= 32 ? 0 : 2);
+#if ZSB_SCAT_SMALLK && ZSB_SCAT_SK  // (not instantiated in the default build)
+    if (sk) {
+        const size_t sbytes = scat_layout(std::min(kmax, 32), PB, 8, 2, SCAT_SK_ITEMS).total;
+        smem_optin(k_scatter_sk<KK, PB>, sbytes);
+        PhaseScope ph(PH_SCATTER, c.st);
+        k_scatter_sk<KK, PB><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles),
+                                                                     kmax <= 32 ? 0 : 1);
+    }
+#endif
+    if (sk && kmax <= 32) {
+    } else if (nset16 == 0) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 8, 2, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
         k_scatter<KK, PB, 8, 2, L1><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
-                                                                        scat_prof(tiles));
+                                                                        scat_prof(tiles), kpart);
     } else if (nset16 == 2) {
         const size_t sbytes = scat_layout(kmax, PB, 16, 2).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 16, 2, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
         k_scatter<KK, PB, 16, 2, L1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
-                                                                         scat_prof(tiles));
+                                                                         scat_prof(tiles), kpart);
     } else {
         const size_t sbytes = scat_layout(kmax, PB, 16, 1).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 16, 1, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
         k_scatter<KK, PB, 16, 1, L1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
-                                                                         scat_prof(tiles));
+                                                                         scat_prof(tiles), kpart);
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
@@ -819,6 +838,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
     int64_t tiles = c.P.ntiles, mat_entries = c.P.k * c.P.ntiles, total_slots = c.P.k + 1, total_windows = nwin1;
     int kmax = (int)c.P.k;
     int level = 1, par = 0;
+    int64_t level_records = n;  // records the level's histogram and scatter pass over
     bool need_stats = true;  // the next level's children need the moments pass (read from classify)
     if (rec) {  // the segment's own stats pass, then the level loop as for a recursion level
         SegAcc a0{~0ull, 0ull, 0.0, 0.0};
@@ -838,6 +858,8 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
         int rc = launch_partition<KK, PB>(c, seg_cur, nseg, tiles, mat_entries, kmax, dst_sel, level == 1,
                                           g_hs.ev_scan);
         if (rc) return rc;
+        g_t.records[PH_HIST] += level_records;
+        g_t.records[PH_SCATTER] += level_records;
         // classify needs the scanned counts, not the scattered records: it runs
         // on the side stream while the scatter runs (C_NCHILD / C_NENTRY were
         // cleared by K2)
@@ -903,6 +925,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
         kmax = (int)hc[C_KMAX_NEXT];
         total_slots = (int64_t)hc[C_NEXT_BIG];
         total_windows = (int64_t)hc[C_WIN_NEXT];
+        level_records = (int64_t)hc[C_REC_NEXT];
         par ^= 1;
         if (mat_entries > c.L.mat_cap) return fail(ZSB_ERR_WORKSPACE, "count matrix overflow");
         if (total_slots > c.L.slot_cap) return fail(ZSB_ERR_WORKSPACE, "bucket slot overflow");
@@ -914,6 +937,7 @@ int run_sort(Ctx &c, const zsb_config &cfg, int64_t *h_stats, const RecStart *re
     fin_prof_dump();
     scat_prof_dump();
 #endif
+    g_t.records[PH_FINISH] += n;  // every record is finished exactly once (finish, team and refine runs)
     return finish_call();
 }
 
@@ -1113,15 +1137,23 @@ int32_t zsb_timing_read(double *ms, int64_t *launches, int32_t nslots, int32_t r
         for (int i = 0; i < PH_SLOTS; i++) {
             g_t.ms[i] = 0;
             g_t.launches[i] = 0;
+            g_t.records[i] = 0;
         }
         g_t.launch_total = 0;
     }
     return PH_SLOTS;
 }
 
+int32_t zsb_timing_records(int64_t *records, int32_t nslots) {
+    int k = nslots < PH_SLOTS ? nslots : PH_SLOTS;
+    for (int i = 0; i < k; i++)
+        if (records) records[i] = g_t.records[i];
+    return PH_SLOTS;
+}
+
 const char *zsb_version(void) {
-    return "zsort_b200 0.1 (sm_100a; K1 moments, K2 hist, K3 lookback scan, K4 token-ring stable scatter, "
-           "K5 smem finish)";
+    return "zsort_b200 0.2 (sm_100a; level-1 sampled CDF map, K2 TMA-ring histogram, K3 look-back scan, "
+           "K4 shared-memory ranked stable scatter, K5 shared-memory finish, K5t team finish, K8 checker)";
 }
 
 size_t zsb_workspace_bytes(int64_t n, int32_t key_dtype, int32_t payload_bytes, const zsb_config *cfg) {

@@ -201,6 +201,29 @@ class TestBuildingBlocks:  # test_core_ops.py with K1/K2/K4 parameter injection
         assert np.array_equal(gk, ek) and np.array_equal(gc, ec)
 
 
+    # fan-outs <= 32 rank by the register multi-split (ballots, no shared
+    # atomics); 33 and 64 take the shared-atomic path with the tie-group loop
+    @pytest.mark.parametrize("k", [2, 3, 16, 17, 31, 32, 33, 64])
+    @pytest.mark.parametrize("kind,n", [("normal", 1_000_003), ("sorted", 300_017), ("few", 50_001), ("normal", 4099)])
+    def test_small_fanout_scatter_vs_oracle(self, Z, k, kind, n):
+        rng = np.random.default_rng(k * 1000 + n % 997)
+        if kind == "normal":
+            keys = (rng.standard_normal(n) * 1e9).astype(np.int64)
+        elif kind == "sorted":  # whole rows of lanes in one bucket, a few displaced records
+            keys = np.sort(rng.integers(-10**12, 10**12, size=n, dtype=np.int64))
+            sw = rng.integers(0, n, size=(n // 50, 2))
+            keys[sw[:, 0]], keys[sw[:, 1]] = keys[sw[:, 1]].copy(), keys[sw[:, 0]].copy()
+        else:
+            keys = rng.choice(np.array([-7, 0, 5, 10**9, -10**9], np.int64), size=n)
+        mean, std, zmin, scale = O.mapping_params(keys, k)
+        params = Z.MappingParams(mean, std, zmin, scale, k)
+        plan = Z.build_partition_plan(keys, params)
+        assert plan.counts.tolist() == O.histogram(keys, mean, std, zmin, scale, k).tolist()
+        gk, gc = Z.stable_scatter(keys, plan, params, np.arange(n, dtype=np.int64))
+        ek, ec, _ = O.stable_scatter(keys, np.arange(n), mean, std, zmin, scale, k)
+        assert np.array_equal(gk, ek) and np.array_equal(gc, ec)
+
+
 # ------------------------------------------------ end to end vs oracle
 
 @pytest.mark.parametrize("mapping", ["fitted", "paper"])
@@ -365,6 +388,29 @@ def test_harness_seam(Z):
     assert np.array_equal(k, ek) and np.array_equal(p, ep)
     r = harness.run_trial_gpu(keys, pay.astype(np.int32), repetitions=3)
     assert r.verified and r.size == keys.size and r.min_ms > 0
+
+
+@pytest.mark.parametrize("kind", ["lognormal", "sorted_swaps", "steps"])
+def test_two_levels_with_small_children(Z, kind):
+    # float64 keys, int32 payload, sized so level 1 leaves children of 2-32
+    # buckets: their scatter ranks by the register multi-split
+    rng = np.random.default_rng(11)
+    n = 3_000_001
+    if kind == "lognormal":
+        keys = rng.lognormal(0.0, 2.0, n)
+    elif kind == "sorted_swaps":
+        keys = np.sort(rng.random(n) * 1e6)
+        sw = rng.integers(0, n, size=(n // 100, 2))
+        keys[sw[:, 0]], keys[sw[:, 1]] = keys[sw[:, 1]].copy(), keys[sw[:, 0]].copy()
+        keys[: n // 2] = rng.lognormal(0.0, 2.0, n // 2)
+    else:  # long runs of equal keys between random stretches
+        keys = np.repeat(rng.standard_normal(n // 1000 + 1), 1000)[:n] + (rng.random(n) < 0.5) * rng.standard_normal(n)
+    pay = np.arange(n, dtype=np.int32)
+    k, p, st = Z.zsort(keys, pay)
+    ek, ep, _ = O.stable_sort(keys, pay)
+    assert np.array_equal(k.view(np.uint64), ek.view(np.uint64)) and np.array_equal(p, ep)
+    if kind == "lognormal":
+        assert st.max_depth_reached >= 2
 
 
 def test_scatter_tie_groups(Z):
