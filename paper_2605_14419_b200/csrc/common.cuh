@@ -148,6 +148,10 @@ enum Ctrl {
     C_SLOTS = 28
 };
 
+#ifndef ZSB_EXP_CHEAPMAP
+#define ZSB_EXP_CHEAPMAP 0
+#endif
+
 // ------------------------------------------------------------ key traits
 
 template <int KK>
@@ -257,6 +261,9 @@ __device__ __forceinline__ int32_t seg_bucket(uint64_t bits, const SegParams &p,
         const float f = floorf(zc_coord(key_value<KK>(bits), p.center, p.za, p.zb));
         return !(f > 0.0f) ? 0 : (f >= (float)p.k ? p.k - 1 : (int32_t)f);
     };
+#if ZSB_EXP_CHEAPMAP  // what-if (wrong output): a conversion-free bucket map, to time the mapping's share
+    if constexpr (BM == 1 || BM == 4) return (int32_t)((bits >> 20) & (uint64_t)(p.k - 1));
+#endif
     if constexpr (BM == 1) {
         return bucket_cdf(key_value<KK>(bits), p, cdf);
     } else if constexpr (BM == 3) {

@@ -2015,9 +2015,13 @@ __global__ void __launch_bounds__(1024) k_classify(const SegParams *__restrict__
 
 constexpr int FIN_INS = 32;         // sub-buckets up to this size are ranked by comparison
 constexpr int FIN_SBITS_MAX = 13;   // <= 8192 sub-buckets (16-bit cursors)
-constexpr int FIN_BIG_MAX = 384;    // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
+#ifndef ZSB_FT
+#define ZSB_FT 1024  // threads per finish CTA; 512: two CTAs per SM with half the run capacity (experiment, needs -DZSB_TEAM=0)
+#endif
+constexpr int FIN_BIG_MAX = ZSB_FT == 1024 ? 384 : 192;  // >= cap / (FIN_INS + 1): every oversized sub-bucket fits
 
-constexpr int FT = 1024;        // threads per finish CTA
+constexpr int FT = ZSB_FT;      // threads per finish CTA
+constexpr int FIN_CTAS = 1024 / FT;  // finish CTAs per SM
 constexpr int FW = FT / 32;     // warps per finish CTA
 
 template <int PB>
@@ -2653,7 +2657,7 @@ __device__ __forceinline__ int team_run(const Buffers &B, const Entry e, int cap
                                         uint32_t &parity, TeamShared &ts) {
     using P = typename PayloadT<PB>::T;
     constexpr int F = FinItems<PB>::F;
-    static_assert(FT == TEAM_NS, "one sample per thread of the splitter sort");
+    static_assert(!TEAM_ON || FT == TEAM_NS, "one sample per thread of the splitter sort");
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cl = cg::this_cluster();
     const FinLayout L = fin_layout(cap, PB);
@@ -2951,7 +2955,7 @@ struct RefineArgs {  // the refine iterations a finish launch runs after its own
 // iterations of the runs it left in `refine`: one launch per level instead
 // of two.
 template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__restrict__ entries,
+__global__ void __launch_bounds__(FT, FIN_CTAS) k_finish(Buffers B, const Entry *__restrict__ entries,
                                                   const unsigned long long *count, int64_t count_const, int cap,
                                                   Entry *refine, unsigned long long *refine_count, int fin_ins,
                                                   long long *prof, unsigned long long *ticket, int prefetch,
@@ -2981,7 +2985,7 @@ __global__ void __launch_bounds__(FT, 1) k_finish(Buffers B, const Entry *__rest
 
 // Refine pass as a launch of its own (cooperative, every CTA resident).
 template <int KK, int PB>
-__global__ void __launch_bounds__(FT, 1) k_refine(Buffers B, Entry *list_a, unsigned long long *count_a, Entry *list_b,
+__global__ void __launch_bounds__(FT, FIN_CTAS) k_refine(Buffers B, Entry *list_a, unsigned long long *count_a, Entry *list_b,
                                                   unsigned long long *count_b, int64_t cap_list, int cap, int fin_ins,
                                                   unsigned long long *ticket, unsigned long long *runs_total,
                                                   int prefetch) {

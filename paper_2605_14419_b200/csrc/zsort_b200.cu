@@ -548,7 +548,7 @@ int launch_finish(Ctx &c, const Entry *list, const unsigned long long *count_dev
     smem_optin(k_finish<KK, PB>, FL.total);
     Entry *refine = (Entry *)(c.ws + c.L.refine[ref_out]);
     unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
-    const int64_t grid = count_dev ? std::min<int64_t>(count_bound, (int64_t)num_sms()) : count_bound;
+    const int64_t grid = count_dev ? std::min<int64_t>(count_bound, (int64_t)num_sms() * FIN_CTAS) : count_bound;
     RefineArgs ra{};
     ra.order = order;
     if (fuse_par >= 0) {
@@ -664,7 +664,7 @@ int launch_refine(Ctx &c, int par) {
     void *args[] = {&Bv, &la, &ca, &lb, &cb, &cl, &cap, &fi, &tick, &tot, &pf};
     {
         PhaseScope ph(PH_FINISH, c.st);
-        ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_refine<KK, PB>, dim3(num_sms()), dim3(FT), args, FL.total,
+        ZSB_CUDA(cudaLaunchCooperativeKernel((const void *)k_refine<KK, PB>, dim3(num_sms() * FIN_CTAS), dim3(FT), args, FL.total,
                                              c.st));
     }
     ZSB_LAUNCH("k_refine");
