@@ -28,6 +28,9 @@ constexpr int NT = 256;        // threads per CTA for the streaming kernels
 #ifndef ZSB_ZLIN
 #define ZSB_ZLIN 1  // fitted recursion levels map with Eq. 1's line in fp32 (MODE_ZLIN, own body)
 #endif
+#ifndef ZSB_SW32
+#define ZSB_SW32 0  // 1: level 1 scatters with 32 warps of 8 records (k_scatter32; experiment)
+#endif
 #ifndef ZSB_HIST_SMALLK
 #define ZSB_HIST_SMALLK 0  // 1: histograms of <= 32 buckets count by ballots (measured slower: C4 level 2 235 -> 290 us)
 #endif
@@ -1184,6 +1187,20 @@ __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const S
     else
         scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
 }
+
+#if ZSB_SW32
+// Experiment (-DZSB_SW32=1): the level-1 scatter with 32 warps of 8 records
+// (the same 8192-record round, one counter set, 64 registers per thread)
+// instead of 16 warps of 16: twice the resident warps behind the ranking chain.
+template <int KK, int PB>
+__global__ void __launch_bounds__(1024, 1) k_scatter32(Buffers B, const SegParams *__restrict__ segs, int nseg,
+                                                       const uint32_t *__restrict__ mat, int dst_sel,
+                                                       long long *prof, int kpart) {
+    const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
+    if (mode == MODE_ZCDF) scatter_body<KK, PB, 32, 1, 1, 8>(B, segs, nseg, mat, dst_sel, prof, kpart);
+    else scatter_body<KK, PB, 32, 0, 1, 8>(B, segs, nseg, mat, dst_sel, prof, kpart);
+}
+#endif
 
 // Recursion levels whose segments all have k <= 32 (children of a 10^8-key
 // level 1, destination ranks): SCAT_SK_ITEMS records per thread and 64

@@ -462,6 +462,13 @@ int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t
     }
 #endif
     if (sk && kmax <= 32) {
+#if ZSB_SW32
+    } else if (L1 && want16 && scat_layout(kmax, PB, 32, 1, 8).total + cdf_bytes <= smax) {
+        const size_t sbytes = scat_layout(kmax, PB, 32, 1, 8).total + cdf_bytes;
+        smem_optin(k_scatter32<KK, PB>, sbytes);
+        PhaseScope ph(PH_SCATTER, c.st);
+        k_scatter32<KK, PB><<<(unsigned)tiles, 1024, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles), kpart);
+#endif
     } else if (nset16 == 0) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 8, 2, L1>, sbytes);
