@@ -28,17 +28,8 @@ constexpr int NT = 256;        // threads per CTA for the streaming kernels
 #ifndef ZSB_ZLIN
 #define ZSB_ZLIN 1  // fitted recursion levels map with Eq. 1's line in fp32 (MODE_ZLIN, own body)
 #endif
-#ifndef ZSB_SW32
-#define ZSB_SW32 0  // 1: level 1 scatters with 32 warps of 8 records (k_scatter32; experiment)
-#endif
-#ifndef ZSB_HIST_SMALLK
-#define ZSB_HIST_SMALLK 0  // 1: histograms of <= 32 buckets count by ballots (measured slower: C4 level 2 235 -> 290 us)
-#endif
 #ifndef ZSB_EXP_NOSTORE
 #define ZSB_EXP_NOSTORE 0  // what-if experiments (wrong results): scatter without its global stores
-#endif
-#ifndef ZSB_EXP_NORANK
-#define ZSB_EXP_NORANK 0   // what-if: scatter without the ranking (rank = item index)
 #endif
 #ifndef ZSB_SCAT_SMALLK
 #define ZSB_SCAT_SMALLK 1  // fan-outs <= 32 rank by a register multi-split (ballots), not shared atomics
@@ -490,30 +481,6 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
         atomicAdd(&hist[bk], 1u);
     };
 
-    // Small fan-outs (recursion children of <= 32 buckets, destination ranks):
-    // 32 lanes on a handful of counters serialise the shared atomics, so the
-    // converged loops count with a warp multi-split in registers (one ballot
-    // per bucket bit: lane b sees the lanes of bucket b) and add once per warp
-    // at the end; the ragged ends keep the atomics.
-    const bool ksmall = BM != 1 && ZSB_HIST_SMALLK && p.k <= 32;
-    const int hlane = threadIdx.x & 31;
-    uint32_t wc = 0;
-    auto count_conv = [&](uint64_t b, int64_t i) {  // called by whole warps only
-        if (ksmall) {
-            const int bk = seg_bucket<KK, BM>(b, p, i, B.cuts, cdf);
-            ZSB_CHECK(bk >= 0 && bk < p.k);
-            unsigned mine = 0xffffffffu;
-#pragma unroll
-            for (int q = 0; q < 5; q++) {
-                const unsigned bal = __ballot_sync(0xffffffffu, (bk >> q) & 1);
-                mine &= ((hlane >> q) & 1) ? bal : ~bal;
-            }
-            wc += (uint32_t)__popc(mine);
-        } else {
-            count(b, i);
-        }
-    };
-
     const uint64_t *tsrc = src + t0;
     int64_t len = t1 - t0;
     if (stage_ok && ((uintptr_t)tsrc & 15) != 0 && len > 0) {  // 8-byte head before the 16-byte-aligned copies
@@ -552,7 +519,7 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
 #pragma unroll
                 for (int u = 0; u < PER; u++) kv[u] = kb[threadIdx.x + u * HT];
                 #pragma unroll
-                for (int u = 0; u < PER; u++) count_conv(kv[u], t0 + c0 + threadIdx.x + u * HT);
+                for (int u = 0; u < PER; u++) count(kv[u], t0 + c0 + threadIdx.x + u * HT);
             } else {
 #pragma unroll 4
                 for (int i = threadIdx.x; i < cfull; i += HT) count(kb[i], t0 + c0 + i);
@@ -569,11 +536,10 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
 #pragma unroll
             for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
             #pragma unroll
-            for (int u = 0; u < 8; u++) count_conv(b[u], i + u * HT);
+            for (int u = 0; u < 8; u++) count(b[u], i + u * HT);
         }
         for (; i < t1; i += HT) count(__ldcs(src + i), i);
     }
-    if (ksmall && hlane < p.k && wc) atomicAdd(&hist[hlane], wc);
     if (__syncthreads_or(nan) && threadIdx.x == 0) *status = 3;  // ZSB_ERR_NAN
     for (int b = threadIdx.x; b < p.k; b += HT) col[(int64_t)b * p.ntiles] = hist[b];
 }
@@ -692,7 +658,10 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 //          (item j of lane l = record w*32*ITEMS + j*32 + l); every item takes
 //          a rank from its per-(warp, bucket) u16 counter with one shared
 //          atomic (ranks follow j; lane ties inside one instruction are
-//          detected by re-reading the counter and re-ranked by a match);
+//          detected by re-reading the counter and re-ranked in lane order,
+//          one tie group per iteration of a ballot loop); segments of at
+//          most 32 buckets rank by a register multi-split instead (ballots
+//          and two shuffles, no shared atomic);
 //   scan   exclusive scan of the counters in (bucket, warp) order;
 //   place  records go to shared memory at (warp, bucket) base + rank;
 //   write  thread i stores staged record i to cursor[b] + (i - run_start[b]):
@@ -707,12 +676,6 @@ __global__ void __launch_bounds__(NT) k_scan(uint32_t *data, int64_t total, unsi
 #endif
 constexpr int SCAT_ITEMS = ZSB_SCAT_ITEMS;
 constexpr int KSCAT_MAX = 2048;  // fan-out limit of one pass
-#ifndef ZSB_SCAT_RUNS
-#define ZSB_SCAT_RUNS 0  // N > 0: rows of at most N runs of equal adjacent buckets add once per run (measured: C4 scatter +1 %, C2 +4 %: the 32-way same-address atomics of ordered inputs are not what bounds the kernel)
-#endif
-#ifndef ZSB_SCAT_TIE_MATCH
-#define ZSB_SCAT_TIE_MATCH 0  // 1: tie groups re-ranked with one MATCH.ANY (round-2 start) instead of a ballot loop
-#endif
 #ifndef ZSB_SCAT_AHEAD
 #define ZSB_SCAT_AHEAD 0  // 1: each item's bucket computed one item ahead of its ranking (measured neutral)
 #endif
@@ -727,8 +690,8 @@ struct ScatLayout {
     size_t off_cur, off_cnt, off_lst, off_k, off_p, off_b, off_cdf, total;
 };
 
-__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw, int nset = 2, int items = SCAT_ITEMS) {
-    const int round = sw * 32 * items;
+__host__ __device__ inline ScatLayout scat_layout(int k, int pb, int sw, int nset = 2) {
+    const int round = sw * 32 * SCAT_ITEMS;
     ScatLayout L;
     size_t o = 0;
     L.off_cur = o;
@@ -834,12 +797,9 @@ __device__ __forceinline__ void scan_wd(uint16_t *cnt, int ndig, uint16_t *dstar
     __syncthreads();
 }
 
-// SK: small-fan-out kernel (k <= 32 in every segment of the launch): only the
-// register multi-split ranking is compiled, ITEMS records per thread.
-template <int KK, int PB, int SW, int BM, int NSET, int ITEMS = SCAT_ITEMS, bool SK = false>
+template <int KK, int PB, int SW, int BM, int NSET>
 __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *__restrict__ segs, int nseg,
-                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof,
-                                             int kpart = 0) {
+                                             const uint32_t *__restrict__ mat, int dst_sel, long long *prof) {
 #ifdef ZSB_PHASE_PROFILE  // per-phase clock64 accounting (build with ZSB_PHASE_PROFILE=1)
     long long t_mark = prof ? clock64() : 0;
     long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
@@ -857,15 +817,13 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
     } while (0)
 #endif
     using P = typename PayloadT<PB>::T;
+    constexpr int ITEMS = SCAT_ITEMS;
     constexpr int ST = SW * 32;             // threads
     constexpr int ROUND = ST * ITEMS;       // records per round
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t wtot[SW];
     int s = find_seg(segs, nseg, blockIdx.x);
     const SegParams p = segs[s];
-    // a level split over two launches: kpart 1 takes the segments of k <= 32
-    // (k_scatter_sk), kpart 2 the others
-    if ((kpart == 1 && p.k > 32) || (kpart == 2 && p.k <= 32)) return;
     const int64_t ti = blockIdx.x - p.tile_first;
     const int64_t t0 = p.start + ti * p.tile_len;
     const int64_t t1 = min(t0 + p.tile_len, p.start + p.len);
@@ -881,7 +839,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         return;
     }
     const int k = p.k;
-    const ScatLayout L = scat_layout(k, PB, SW, NSET, ITEMS);
+    const ScatLayout L = scat_layout(k, PB, SW, NSET);
     const int NC = k * SW;
     uint32_t *cur = (uint32_t *)(smem + L.off_cur);
     uint16_t *cnt2 = (uint16_t *)(smem + L.off_cnt);  // [NSET][SW][k]
@@ -943,12 +901,16 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
         // share a bucket -- a tie group -- may get their counts in any order:
         // the converged warp re-reads its counters after the atomic, a group
         // of g lanes finds the group start + g there, and every such group is
-        // re-ranked in lane order with a match -- the checked path, always
-        // on, paid only by instructions holding a tie group.  Interleaved with
-        // the coalesced write of staged slot tid + j*ST of the previous round.
-        // (Measured on B200 and not used: a ballot-per-bucket-bit multi-split
-        // with no re-read, 27 % slower; a second __syncwarp between the atomic
-        // and the re-read, 8 % slower.)
+        // re-ranked in lane order, one group per iteration of a ballot loop --
+        // the checked path, always on, paid only by instructions holding a tie
+        // group.  Interleaved with the coalesced write of staged slot
+        // tid + j*ST of the previous round.
+        // (Measured on B200 and not used at 1024 buckets: a ballot-per-bucket-
+        // bit multi-split with no re-read, 27 % slower -- it is the path of
+        // fan-outs <= 32, five ballots; one MATCH.ANY per tie row instead of
+        // the loop, C4 +2 %; a second __syncwarp between the atomic and the
+        // re-read, 8 % slower; one atomic per run of equal adjacent buckets
+        // for ordered inputs, no gain.)
         uint32_t pk[ITEMS];  // bucket | rank << 16
         // (Measured and not used: computing every item's bucket and the
         // previous round's writes in a barrier-free loop before the ranking
@@ -976,14 +938,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 }
             }
         };
-        if (ZSB_EXP_NORANK) {
-#pragma unroll
-            for (int j = 0; j < ITEMS; j++) {
-                const int bkj = bucket_of_item(j);
-                pk[j] = bkj >= 0 ? (uint32_t)bkj | ((uint32_t)j << 16) : 0xffffffffu;
-                write_prev(j);
-            }
-        } else if (SK || (BM != 1 && SW == 8 && ZSB_SCAT_SMALLK && k <= 32)) {  // (8-warp kernels: kmax <= 512)
+        if (BM != 1 && SW == 8 && ZSB_SCAT_SMALLK && k <= 32) {  // (8-warp kernels: kmax <= 512)
             // Small fan-out (recursion children, destination ranks): every
             // instruction holds many lanes per bucket, so the ranking is a warp
             // multi-split in registers -- one ballot per bucket bit gives lane b
@@ -1012,7 +967,7 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 write_prev(j);
             }
             if (lane < k) cnt[w * k + lane] = (uint16_t)wc;
-        } else if constexpr (!SK) {
+        } else {
             // the next item's bucket (its mapping-table load) is computed ahead,
             // before this item's warp barrier, so it overlaps the ranking chain
             int bk_next = ZSB_SCAT_AHEAD ? bucket_of_item(0) : 0;
@@ -1031,61 +986,10 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                 const uint32_t sh = 16 * (q & 1);
                 uint32_t *word = (uint32_t *)cnt + (q >> 1);
                 __syncwarp();  // item j - 1's re-reads before item j's atomics
-#if ZSB_SCAT_RUNS
-                // Ordered inputs put whole rows of lanes in one bucket, and 32
-                // lanes on one counter serialise the shared atomic into 32
-                // passes (ncu: 17 wavefronts per atomic on config 4, 41 % of the
-                // kernel's shared-memory traffic).  A row made of few runs of
-                // equal adjacent buckets adds once per run -- the run's head
-                // adds its length and hands count and re-read to its lanes;
-                // two runs of one bucket in a row meet as a tie group below.
-                const int prevb = __shfl_up_sync(0xffffffffu, bkj, 1);
-                const unsigned hm = __ballot_sync(0xffffffffu, lane == 0 || bkj != prevb);
-                bool tie;
-                if (__popc(hm) <= ZSB_SCAT_RUNS) {
-                    const int hl = 31 - __clz(hm & (lt | (1u << lane)));  // this lane's run head
-                    const unsigned nx = hm & ~(lt | (1u << lane));        // heads after this lane
-                    const uint32_t len = (uint32_t)((nx ? __ffs(nx) - 1 : 32) - hl);
-                    bool th = false;
-                    if (v && lane == hl) {
-                        old = (atomicAdd(word, len << sh) >> sh) & 0xFFFFu;
-                        after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
-                        th = after != old + len;
-                    }
-                    const unsigned tmh = __ballot_sync(0xffffffffu, th);
-                    old = __shfl_sync(0xffffffffu, old, hl) + (uint32_t)(lane - hl);
-                    after = __shfl_sync(0xffffffffu, after, hl);
-                    tie = v && ((tmh >> hl) & 1u);
-                } else {
-                    if (v) {
-                        old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
-                        after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
-                    }
-                    tie = v && after != old + 1u;
-                }
-                {
-                    unsigned tm = __ballot_sync(0xffffffffu, tie);
-                    while (tm) {
-                        const int bl = __shfl_sync(0xffffffffu, bkj, __ffs(tm) - 1);
-                        const unsigned grp = __ballot_sync(0xffffffffu, bkj == bl);
-                        if (bkj == bl) old = after - (uint32_t)__popc(grp) + (uint32_t)__popc(grp & lt);
-                        tm &= ~grp;
-                    }
-                }
-#else
                 if (v) {
                     old = (atomicAdd(word, 1u << sh) >> sh) & 0xFFFFu;
                     after = (*(volatile uint32_t *)word >> sh) & 0xFFFFu;
                 }
-#if ZSB_SCAT_TIE_MATCH
-                {
-                    const bool tie = v && after != old + 1u;
-                    if (__any_sync(0xffffffffu, tie)) {
-                        const unsigned m = __match_any_sync(0xffffffffu, bkj);
-                        if (v && (m & (m - 1u))) old = after - (uint32_t)__popc(m) + (uint32_t)__popc(m & lt);
-                    }
-                }
-#else
                 {
                     // tie groups one at a time (a MATCH.ANY occupies the SM for
                     // ~64 cycles; a group costs two ballots and a shuffle): all
@@ -1100,8 +1004,6 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
                         tm &= ~grp;
                     }
                 }
-#endif
-#endif
                 pk[j] = v ? (uint32_t)bkj | (old << 16) : 0xffffffffu;
                 write_prev(j);
             }
@@ -1174,57 +1076,18 @@ __device__ __forceinline__ void scatter_body(const Buffers &B, const SegParams *
 template <int KK, int PB, int SW, int NSET, int L1>
 __global__ void __launch_bounds__(SW * 32, 16 / SW) k_scatter(Buffers B, const SegParams *__restrict__ segs,
                                                               int nseg, const uint32_t *__restrict__ mat,
-                                                              int dst_sel, long long *prof, int kpart) {
+                                                              int dst_sel, long long *prof) {
     const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
     if (L1 && mode == MODE_ZCDF)
-        scatter_body<KK, PB, SW, 1, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
+        scatter_body<KK, PB, SW, 1, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else if (!L1 && ZSB_BM_ZSCORE && mode == MODE_ZSCORE)
-        scatter_body<KK, PB, SW, 3, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
+        scatter_body<KK, PB, SW, 3, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else if (!L1 && ZSB_ZLIN && mode == MODE_ZLIN)
-        scatter_body<KK, PB, SW, 4, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
+        scatter_body<KK, PB, SW, 4, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else if (!L1 && mode == MODE_DEST && B.peers)
-        scatter_body<KK, PB, SW, 5, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
+        scatter_body<KK, PB, SW, 5, NSET>(B, segs, nseg, mat, dst_sel, prof);
     else
-        scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof, kpart);
-}
-
-#if ZSB_SW32
-// Experiment (-DZSB_SW32=1): the level-1 scatter with 32 warps of 8 records
-// (the same 8192-record round, one counter set, 64 registers per thread)
-// instead of 16 warps of 16: twice the resident warps behind the ranking chain.
-template <int KK, int PB>
-__global__ void __launch_bounds__(1024, 1) k_scatter32(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                                       const uint32_t *__restrict__ mat, int dst_sel,
-                                                       long long *prof, int kpart) {
-    const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
-    if (mode == MODE_ZCDF) scatter_body<KK, PB, 32, 1, 1, 8>(B, segs, nseg, mat, dst_sel, prof, kpart);
-    else scatter_body<KK, PB, 32, 0, 1, 8>(B, segs, nseg, mat, dst_sel, prof, kpart);
-}
-#endif
-
-// Recursion levels whose segments all have k <= 32 (children of a 10^8-key
-// level 1, destination ranks): SCAT_SK_ITEMS records per thread and 64
-// registers, four CTAs of 8 warps per SM (2048-record rounds: runs of >= 64
-// records per bucket), ranking by the register multi-split only.
-#ifndef ZSB_SCAT_SK_ITEMS
-#define ZSB_SCAT_SK_ITEMS 8
-#endif
-constexpr int SCAT_SK_ITEMS = ZSB_SCAT_SK_ITEMS;
-constexpr int SCAT_SK_CTAS = 32 / SCAT_SK_ITEMS;  // per SM
-
-template <int KK, int PB>
-__global__ void __launch_bounds__(256, SCAT_SK_CTAS) k_scatter_sk(Buffers B, const SegParams *__restrict__ segs, int nseg,
-                                                                 const uint32_t *__restrict__ mat, int dst_sel,
-                                                                 long long *prof, int kpart) {
-    const int mode = segs[find_seg(segs, nseg, blockIdx.x)].mode;
-    if (ZSB_BM_ZSCORE && mode == MODE_ZSCORE)
-        scatter_body<KK, PB, 8, 3, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
-    else if (ZSB_ZLIN && mode == MODE_ZLIN)
-        scatter_body<KK, PB, 8, 4, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
-    else if (mode == MODE_DEST && B.peers)
-        scatter_body<KK, PB, 8, 5, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
-    else
-        scatter_body<KK, PB, 8, 0, 2, SCAT_SK_ITEMS, true>(B, segs, nseg, mat, dst_sel, prof, kpart);
+        scatter_body<KK, PB, SW, 0, NSET>(B, segs, nseg, mat, dst_sel, prof);
 }
 
 // ------------------------------------------------------- equalisation

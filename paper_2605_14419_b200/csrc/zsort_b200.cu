@@ -128,9 +128,6 @@ void timing_collect() {
 #ifndef ZSB_K1_TEAM
 #define ZSB_K1_TEAM 2048  // cap on the level-1 bucket count when buckets are sized for team runs
 #endif
-#ifndef ZSB_SCAT_SK
-#define ZSB_SCAT_SK 0  // 1: recursion-level segments of k <= 32 run k_scatter_sk (8 records per thread, 4 CTAs per SM; measured: no faster, the split launch costs C4 +0.1 ms)
-#endif
 #ifndef ZSB_SW16_ABOVE
 #define ZSB_SW16_ABOVE 512  // bucket counts above this use 16-warp, 8192-record scatter rounds
 #endif
@@ -447,46 +444,24 @@ int launch_partition_l(Ctx &c, SegParams *segs, int nseg, int64_t tiles, int64_t
     const bool want16 = scat_warps(kmax, ZSB_SW16_ABOVE) == 16;
     const int nset16 = !want16 ? 0 : (scat_layout(kmax, PB, 16, 2).total + cdf_bytes <= smax ? 2
                                        : (scat_layout(kmax, PB, 16, 1).total + cdf_bytes <= smax ? 1 : 0));
-    // recursion levels: the segments of k <= 32 go through k_scatter_sk; a level
-    // that also holds larger fan-outs is split over two launches (each CTA
-    // exits at once on a tile of the other part)
-    const bool sk = !L1 && ZSB_SCAT_SMALLK && ZSB_SCAT_SK;
-    const int kpart = !sk ? 0 : (kmax <= 32 ? 0 : 2);
-#if ZSB_SCAT_SMALLK && ZSB_SCAT_SK  // (not instantiated in the default build)
-    if (sk) {
-        const size_t sbytes = scat_layout(std::min(kmax, 32), PB, 8, 2, SCAT_SK_ITEMS).total;
-        smem_optin(k_scatter_sk<KK, PB>, sbytes);
-        PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter_sk<KK, PB><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles),
-                                                                     kmax <= 32 ? 0 : 1);
-    }
-#endif
-    if (sk && kmax <= 32) {
-#if ZSB_SW32
-    } else if (L1 && want16 && scat_layout(kmax, PB, 32, 1, 8).total + cdf_bytes <= smax) {
-        const size_t sbytes = scat_layout(kmax, PB, 32, 1, 8).total + cdf_bytes;
-        smem_optin(k_scatter32<KK, PB>, sbytes);
-        PhaseScope ph(PH_SCATTER, c.st);
-        k_scatter32<KK, PB><<<(unsigned)tiles, 1024, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel, scat_prof(tiles), kpart);
-#endif
-    } else if (nset16 == 0) {
+    if (nset16 == 0) {
         const size_t sbytes = scat_layout(kmax, PB, 8).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 8, 2, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
         k_scatter<KK, PB, 8, 2, L1><<<(unsigned)tiles, 256, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
-                                                                        scat_prof(tiles), kpart);
+                                                                        scat_prof(tiles));
     } else if (nset16 == 2) {
         const size_t sbytes = scat_layout(kmax, PB, 16, 2).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 16, 2, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
         k_scatter<KK, PB, 16, 2, L1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
-                                                                         scat_prof(tiles), kpart);
+                                                                         scat_prof(tiles));
     } else {
         const size_t sbytes = scat_layout(kmax, PB, 16, 1).total + cdf_bytes;
         smem_optin(k_scatter<KK, PB, 16, 1, L1>, sbytes);
         PhaseScope ph(PH_SCATTER, c.st);
         k_scatter<KK, PB, 16, 1, L1><<<(unsigned)tiles, 512, sbytes, c.st>>>(c.B, segs, nseg, mat, dst_sel,
-                                                                         scat_prof(tiles), kpart);
+                                                                         scat_prof(tiles));
     }
     ZSB_LAUNCH("k_scatter");
     return ZSB_OK;
