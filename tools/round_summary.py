@@ -1,4 +1,4 @@
-"""profiles/<tag>_summary.md (+ bench line, launch list, traffic json, pytest log) from a tools/gpu_s4j.sh run.
+"""profiles/<tag>_summary.md (+ bench line, launch list, traffic json, pytest log) from a tools/gpu_round_evidence.sh run.
 
 usage: python tools/round_summary.py TAG"""
 import json
