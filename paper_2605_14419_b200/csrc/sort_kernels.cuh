@@ -31,6 +31,9 @@ constexpr int NT = 256;        // threads per CTA for the streaming kernels
 #ifndef ZSB_EXP_NOSTORE
 #define ZSB_EXP_NOSTORE 0  // what-if experiments (wrong results): scatter without its global stores
 #endif
+#ifndef ZSB_HIST_UNROLL
+#define ZSB_HIST_UNROLL 8  // keys per thread in flight in the recursion-level histogram (per-thread loads)
+#endif
 #ifndef ZSB_SCAT_SMALLK
 #define ZSB_SCAT_SMALLK 1  // fan-outs <= 32 rank by a register multi-split (ballots), not shared atomics
 #endif
@@ -531,12 +534,13 @@ __device__ __forceinline__ void hist_body(const Buffers &B, const SegParams *__r
     } else {
         __syncthreads();
         int64_t i = t0 + threadIdx.x;
-        for (int64_t ib = t0; ib + 8 * HT <= t1; ib += 8 * HT, i += 8 * HT) {  // CTA-uniform trip count
-            uint64_t b[8];
+        constexpr int HU = ZSB_HIST_UNROLL;  // keys per thread in flight
+        for (int64_t ib = t0; ib + HU * HT <= t1; ib += HU * HT, i += HU * HT) {  // CTA-uniform trip count
+            uint64_t b[HU];
 #pragma unroll
-            for (int u = 0; u < 8; u++) b[u] = __ldcs(src + i + u * HT);
+            for (int u = 0; u < HU; u++) b[u] = __ldcs(src + i + u * HT);
             #pragma unroll
-            for (int u = 0; u < 8; u++) count(b[u], i + u * HT);
+            for (int u = 0; u < HU; u++) count(b[u], i + u * HT);
         }
         for (; i < t1; i += HT) count(__ldcs(src + i), i);
     }
