@@ -49,7 +49,11 @@ class SortPipeline:
     download).  ``submit`` enqueues the upload at once and launches the sort
     of the *previous* ticket behind it: the library's sort call holds the
     host until the last partition level is enqueued (one wait per level), so
-    the next upload has to be in flight before that call starts."""
+    the next upload has to be in flight before that call starts.  A ticket's
+    host tensors belong to the pipeline until ``wait(ticket)`` returns.  One
+    pipeline per host thread (the object itself is not thread-safe; separate
+    pipelines on separate threads are independent, like separate ``zsort``
+    calls)."""
 
     def __init__(self, n, key_dtype, payload_dtype=None, config: SortConfig | None = None, depth: int = 2,
                  device=None):
