@@ -1074,6 +1074,8 @@ struct PartitionOp {
         SegParams *seg = (SegParams *)(c.ws + c.L.seg_a);
         unsigned long long *ctrl = (unsigned long long *)(c.ws + c.L.ctrl);
         if (phases & 1) ZSB_CUDA(cudaMemsetAsync(ctrl, 0, C_SLOTS * 8, c.st));
+        if (phases & 1) g_t.records[PH_HIST] += c.n;     // the shard's records pass through each phase once
+        if (phases & 2) g_t.records[PH_SCATTER] += c.n;
         return launch_partition_l<KK, PB, 0>(c, seg, 1, c.P.ntiles, c.P.k * c.P.ntiles, (int)c.P.k, 2, false, nullptr,
                                              phases);
     }
